@@ -1,0 +1,362 @@
+"""Benchmark: chunked prefill tokens/s on configs[1] (B=8, H=32, N=8192, d=128, bf16).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one pass of the hot path over one batch: a single chunked-prefill
+launch over [B, H, N, d] bf16 Q/K/V already resident in HBM (``value``), and
+the same call through the public API with pinned HOST buffers, H2D + D2H inside
+the timed region (``e2e``).  Multi-GPU: one process per GPU (torchrun), batch x
+head sharding with no data-path collective -> each rank runs the full configs[1]
+batch ("scaling": "weak"); the timed region is bracketed by barrier +
+synchronize and the max over ranks is reported.
+
+Extra keys: ``roofline`` (dominant kernel vs MEASURED_PEAKS.json), ``cpu_baseline``
+(the oracle port of the reference's CPU blocking route on a bounded sample,
+rank 0 only), ``decode`` (configs[3] decode step), ``clocks`` (nvidia-smi during
+the timed region), ``gpu_launches`` (our kernels launched in the timed region).
+``--impl reference`` times the reference's CPU algorithm (oracle port; the
+reference is pure Python/numpy and cannot travel to the GPU box) on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mproc
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prefill tokens/s @N=8K,d=128 bf16 (% TC peak); decode-step us & HBM GB/s"
+CFG = dict(B=8, H=32, N=8192, dk=128, dv=128)           # BASELINE.json configs[1]
+DEC = dict(B=256, H=32, dk=128, dv=128, steps=1024)     # BASELINE.json configs[3]
+C0 = 64                                                  # reference default chunk (kernels.py:57)
+
+
+def gammas(h):
+    """Per-head gamma_h = 1 - 2^(-5 - 10 h / (H-1))."""
+    return [1.0 - 2.0 ** (-5 - 10 * i / max(1, h - 1)) for i in range(h)]
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", 0)), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# --------------------------------------------------------------------------- CPU arm
+
+def _cpu_slice(args):
+    """One (b, h) slice of the reference CPU blocking route, f32 (oracle port)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import linattn_oracle as orc
+    n, dk, dv, gamma, seed = args
+    rng = np.random.default_rng(seed)
+    b = rng.standard_normal((1, 1, n, dk)).astype(np.float32)
+    c = rng.standard_normal((1, 1, n, dk)).astype(np.float32)
+    v = rng.standard_normal((1, 1, n, dv)).astype(np.float32)
+    t0 = time.perf_counter()
+    orc.blocked_attn(b, c, v, [gamma], True, block=C0)
+    return time.perf_counter() - t0
+
+
+def cpu_sample(pool, cores, per_core=1, seed=0):
+    """Time cores*per_core slices of configs[1] in a process pool; tokens/s equivalent."""
+    g = gammas(CFG["H"])
+    jobs = [(CFG["N"], CFG["dk"], CFG["dv"], g[i % CFG["H"]], seed + i) for i in range(cores * per_core)]
+    t0 = time.perf_counter()
+    pool.map(_cpu_slice, jobs, chunksize=1)
+    dt = time.perf_counter() - t0
+    slices = len(jobs)
+    tokens = slices / (CFG["B"] * CFG["H"]) * CFG["B"] * CFG["N"]  # a token passes through all H heads
+    return tokens / dt, dt, slices
+
+
+def cores_available():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = cores_available()
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ctx = mproc.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        for _ in range(args.warmup):
+            cpu_sample(pool, cores)
+        vals, times = [], []
+        for i in range(args.steps):
+            v, dt, slices = cpu_sample(pool, cores, seed=1000 + i)
+            vals.append(v)
+            times.append(dt)
+    value = float(np.mean(vals))
+    sample = (f"{slices} of {CFG['B'] * CFG['H']} (b,h) slices of configs[1] per step, f32, "
+              f"two-level-block chunk {C0}, process pool x{cores}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "configs[1] chunked prefill B=8,H=32,N=8192,d=128 (bounded CPU sample)",
+                   "global_batch": CFG["B"], "seq_len": CFG["N"], "parallelism": "cpu-process-pool"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+class ClockSampler:
+    """SM clock and throttle reasons sampled (NVML, every 5 ms) during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = None
+
+    def _run(self):
+        import pynvml
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for name, bit in self.REASONS.items():
+                if mask & bit:
+                    self.reasons.add(name)
+            self._stop.wait(0.005)
+
+    def __enter__(self):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+        except Exception:  # no NVML: report no samples rather than fail the bench
+            return self
+        self._stop = threading.Event()
+        self._thread = threading.Thread(target=self._run, daemon=True)
+        self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._stop is not None:
+            self._stop.set()
+            self._thread.join()
+
+    def summary(self):
+        sm = self.samples
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml, 5 ms"}
+
+
+def load_profile_traffic(kernel_key):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(kernel_key, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_02573_b200 import _lib, ops
+    import paper_2501_02573_b200 as la
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    hbm, tc_burst, tc_sus, peak_kind = peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    B, H, N, dk, dv = CFG["B"], CFG["H"], CFG["N"], CFG["dk"], CFG["dv"]
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q = torch.randn(B, H, N, dk, device=dev, dtype=torch.bfloat16, generator=g)
+    k = torch.randn(B, H, N, dk, device=dev, dtype=torch.bfloat16, generator=g)
+    v = torch.randn(B, H, N, dv, device=dev, dtype=torch.bfloat16, generator=g)
+    gam = gammas(H)
+    l2 = ops.log2_gamma(gam, True, dev)
+    out = torch.empty_like(v)
+    kernel = os.environ.get("LINATTN_BENCH_KERNEL", "auto")
+
+    def step():
+        ops.prefill(q, k, v, l2, out=out, kernel=kernel)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = _lib.launch_count() - launches0
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    tokens_per_rank = B * N
+    value = world * tokens_per_rank / (ms * 1e-3)
+
+    # roofline of the dominant (only) kernel in the step: algorithmic bytes / launch duration
+    bytes_launch = B * H * N * ops.bytes_per_token_head(dk, dv)
+    flops_launch = 2 * B * H * N * (C0 * (dk + dv) + 2 * dk * dv)
+    achieved_gbs = bytes_launch / (ms * 1e-3) / 1e9
+    tflops = flops_launch / (ms * 1e-3) / 1e12
+
+    # e2e: public API with pinned host buffers, H2D + kernel + D2H in the timed region
+    e2e_steps = max(1, min(args.steps, 5))
+    qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
+    oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    inputs = la.AttnInputs(b=qh, c=kh, v=vh, gamma=gam, decay=True)
+    la.run_method(la.MethodId.B200_CHUNKED, inputs, validate=False, out=oh)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        la.run_method(la.MethodId.B200_CHUNKED, inputs, validate=False, out=oh)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    del qh, kh, vh, oh, inputs
+
+    # decode step (configs[3]): 1024 single-token steps, state 256x32x128x128 fp32 (512 MiB)
+    dec = None
+    if not args.no_decode:
+        DB, DH, ddk, ddv, T = DEC["B"], DEC["H"], DEC["dk"], DEC["dv"], DEC["steps"]
+        state = torch.zeros(DB, DH, ddk, ddv, device=dev, dtype=torch.float32)
+        qd = torch.randn(DB, DH, ddk, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
+        kd = torch.randn(DB, DH, ddk, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
+        vd = torch.randn(DB, DH, ddv, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
+        od = torch.empty_like(vd)
+        l2d = ops.log2_gamma(gammas(DH), True, dev)
+        for _ in range(3):
+            ops.decode_step(qd, kd, vd, state, l2d, out=od)
+        torch.cuda.synchronize()
+        per_graph = 64
+        graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(graph, stream=s):
+                for _ in range(per_graph):
+                    ops.decode_step(qd, kd, vd, state, l2d, out=od)
+        torch.cuda.current_stream().wait_stream(s)
+        graph.replay()
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        d0.record()
+        for _ in range(T // per_graph):
+            graph.replay()
+        d1.record()
+        torch.cuda.synchronize()
+        us = max_over_ranks(d0.elapsed_time(d1) * 1e3 / T)
+        dbytes = DB * DH * (2 * 4 * ddk * ddv + 2 * (2 * ddk + 2 * ddv))
+        gbs = dbytes / (us * 1e-6) / 1e9
+        dec = {"workload": "configs[3] decode step B=256,H=32,d=128, fp32 state, bf16 q/k/v/o, 1024 steps "
+                           "(CUDA graph of 64 steps)",
+               "us_per_step": us, "hbm_gbs": gbs, "frac_of_hbm": gbs / hbm,
+               "bytes_per_step": dbytes, "steps": T}
+        del state, qd, kd, vd, od
+
+    # CPU baseline (oracle port of the reference's CPU blocking route), rank 0 at N=1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = cores_available()
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        with mproc.get_context("spawn").Pool(cores) as pool:
+            cpu_sample(pool, cores)
+            cv, cdt, slices = cpu_sample(pool, cores, per_core=2, seed=77)
+        cpu = {"value": cv, "unit": "tokens/s", "cores": cores, "kind": "port",
+               "sample": f"{slices} of {B * H} (b,h) slices of configs[1], f32 two-level-block chunk {C0} "
+                         f"(oracle/linattn_oracle.py), process pool x{cores}, {cdt:.1f} s"}
+
+    kernel_name = ops.prefill_kernel_name(dk, dv, torch.bfloat16, kernel)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn bf16, seeded)",
+        "config": {"workload": "configs[1] chunked prefill B=8,H=32,N=8192,dk=dv=128 per GPU",
+                   "global_batch": B * world, "seq_len": N, "heads": H, "parallelism": f"batch x head, {world} rank(s)",
+                   "gamma": "1-2^(-5-10h/(H-1))", "l2": "no flush: 1.5 GiB of inputs per step > 126 MB L2",
+                   "kernel": kernel_name},
+        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved_gbs / hbm, "traffic": load_profile_traffic(kernel_name),
+                     "peak_kind": peak_kind, "bytes_per_launch": bytes_launch,
+                     "tensor_tflops_c64": tflops, "tensor_frac_of_burst": tflops / tc_burst},
+        "e2e": {"value": world * tokens_per_rank / e2e_s, "unit": "tokens/s",
+                "h2d_bytes_per_step": 3 * B * H * N * dk * 2, "d2h_bytes_per_step": B * H * N * dv * 2,
+                "ms_per_step": e2e_s * 1e3, "api": "run_method(b200-chunked) on pinned host bf16 tensors"},
+        "gpu_launches": int(max_over_ranks(launches)),
+        "clocks": clk.summary(),
+        "decode": dec,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,116 @@
+/*
+ * linattn_b200.h -- C ABI of the B200 (sm_100a) decayed causal linear-attention path.
+ *
+ *   O = (Q K^T (.) M_gamma) V,   M_gamma[i, j] = gamma^(i - j) for i >= j, else 0,
+ *   one gamma per head; gamma^0 == 1 even for gamma == 0.
+ *
+ * Reference being replaced (paths relative to /root/reference/pkg/src/linattn):
+ *   linattn_prefill       <- run_method(...) over the CPU blocking routes
+ *                            _block_based_slice (kernels.py:109-136) and
+ *                            _two_level_block_slice (kernels.py:139-166), driven by the
+ *                            batch x head loop of run_method (kernels.py:257-281)
+ *   linattn_decode_step   <- one iteration of _row_based_slice (kernels.py:100-104)
+ *   linattn_state_pass    <- the decayed block carry u <- gamma^L u + (w_rev c)^T v
+ *                            (kernels.py:127-128), i.e. the recursion factor
+ *                            (w2 (.) C1)^T V1 (kernels.py:187-188)
+ *   linattn_prefix_combine<- the recursion cross-term weights (kernels.py:185-189)
+ *                            applied across sequence segments (new: SP prefix)
+ *
+ * The reference's slice kernels take one (N, r) slice; this ABI takes whole
+ * (B, H, N, .) tensors at run_method granularity.
+ *
+ * Conventions
+ *   - q, k: [B, H, N, dk]; v, o: [B, H, N, dv]; contiguous, row-major, DEVICE pointers.
+ *     (reference names: q = B, k = C, dk = rank r, dv = dim d; tensor.py:62-94)
+ *   - states (s_in, s_out, state): [B, H, dk, dv] fp32, device pointers, nullable where noted.
+ *   - log2g: [H] fp32 DEVICE pointer, log2(gamma_h) computed in f64 on the host
+ *     (-inf for gamma == 0, 0 for gamma == 1 or for the binary mask decay=False).
+ *   - dtype: LINATTN_F32 or LINATTN_BF16, for q/k/v/o alike.
+ *   - stream: a cudaStream_t passed as void* (0 = legacy default stream).
+ *   - all calls are stream-ordered and asynchronous; no implicit synchronisation.
+ *   - calls are reentrant; the only process state is per-device kernel attributes
+ *     (set once) and a thread-local error string.
+ *
+ * Status codes map onto the reference exception classes (errors.py:4-29):
+ *   ESHAPE -> ShapeError, EPARAM -> ParameterError, EDTYPE/EUNSUPPORTED -> UsageError,
+ *   ECUDA -> LinAttnError.
+ */
+#ifndef LINATTN_B200_H
+#define LINATTN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LINATTN_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define LINATTN_API __attribute__((visibility("default")))
+#else
+#define LINATTN_API
+#endif
+
+typedef enum {
+  LINATTN_OK = 0,
+  LINATTN_ESHAPE = 1,
+  LINATTN_EPARAM = 2,
+  LINATTN_EDTYPE = 3,
+  LINATTN_EUNSUPPORTED = 4,
+  LINATTN_ECUDA = 5
+} linattn_status;
+
+typedef enum { LINATTN_F32 = 0, LINATTN_BF16 = 1 } linattn_dtype;
+
+/* Kernel family selector for linattn_prefill / linattn_state_pass. */
+typedef enum {
+  LINATTN_KERNEL_AUTO = 0, /* tensor-core kernel when the shape/dtype allows, else SIMT */
+  LINATTN_KERNEL_TC = 1,   /* tcgen05 + TMA chunked kernel (bf16 only); EUNSUPPORTED otherwise */
+  LINATTN_KERNEL_SIMT = 2  /* fp32-FFMA chunked kernel (f32 parity mode; any dk, dv) */
+} linattn_kernel;
+
+/* Chunked prefill.  Optional s_in seeds the recurrence (nullptr = zero state, the
+ * reference behaviour, kernels.py:114/144); optional s_out receives the end state
+ * S_N = sum_j gamma^(N-1-j) k_j^T v_j (+ gamma^N s_in). */
+LINATTN_API int linattn_prefill(const void* q, const void* k, const void* v, void* o,
+                    const float* log2g, const float* s_in, float* s_out,
+                    int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv,
+                    int dtype, int kernel, void* stream);
+
+/* Segment end state from K and V only (no Q, no O): s_out = sum_t gamma^(N-1-t) k_t^T v_t. */
+LINATTN_API int linattn_state_pass(const void* k, const void* v, float* s_out, const float* log2g,
+                       int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv,
+                       int dtype, int kernel, void* stream);
+
+/* Exclusive gamma-weighted prefix of gathered segment end states (sequence parallelism):
+ *   gathered: [P, B, H, dk, dv] fp32 (device); seg_lens: [P] (HOST array);
+ *   s_in = sum_{q < rank} gamma^(sum_{q < m < rank} L_m) * gathered[q]. */
+LINATTN_API int linattn_prefix_combine(const float* gathered, float* s_in, const int64_t* seg_lens,
+                           int P, int rank, const float* log2g,
+                           int64_t B, int64_t H, int64_t dk, int64_t dv, void* stream);
+
+/* One recurrent decode step for a batch of single tokens:
+ *   q, k: [B, H, dk]; v, o: [B, H, dv]; state: [B, H, dk, dv] fp32 updated in place:
+ *   S <- gamma S + k^T v ;  o = q S   (update first, then read: kernels.py:100-104). */
+LINATTN_API int linattn_decode_step(const void* q, const void* k, const void* v, void* o, float* state,
+                        const float* log2g, int64_t B, int64_t H, int64_t dk, int64_t dv,
+                        int dtype, void* stream);
+
+/* Kernel family LINATTN_KERNEL_AUTO resolves to for this shape/dtype (TC or SIMT). */
+LINATTN_API int linattn_prefill_kernel(int64_t dk, int64_t dv, int dtype);
+
+/* Thread-local message for the last non-OK status returned on this thread. */
+LINATTN_API const char* linattn_last_error(void);
+
+/* LINATTN_ABI_VERSION of the loaded library. */
+LINATTN_API int linattn_abi_version(void);
+
+/* Number of kernels this library launched on this thread since load (evidence counter). */
+LINATTN_API int64_t linattn_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LINATTN_B200_H */

@@ -1,0 +1,72 @@
+// K5 (combine half): exclusive gamma-weighted prefix of gathered segment end states.
+//   s_in = sum_{q < rank} gamma^(sum_{q < m < rank} L_m) * S_q
+// evaluated as the scan acc <- gamma^(L_q) acc + S_q over q = 0 .. rank-1 (the
+// recursion cross-term weights of the reference, kernels.py:185-189, applied
+// across sequence segments).  Elementwise over [B, H, dk, dv]; float4 accesses.
+#include "common.cuh"
+
+namespace linattn {
+namespace {
+
+constexpr int MAXP = 64;
+struct SegLens {
+  float len[MAXP];
+};
+
+__global__ void prefix_combine_kernel(const float4* __restrict__ gathered, float4* __restrict__ s_in,
+                                      SegLens lens, int rank, const float* __restrict__ log2g,
+                                      int H, int64_t per_head4, int64_t per_rank4) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= per_rank4) return;
+  const int h = (int)((idx / per_head4) % H);
+  const float lg = log2g[h];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int p = 0; p < rank; ++p) {
+    const float c = gpow(lg, lens.len[p]);
+    const float4 x = gathered[(int64_t)p * per_rank4 + idx];
+    acc.x = fmaf(c, acc.x, x.x);
+    acc.y = fmaf(c, acc.y, x.y);
+    acc.z = fmaf(c, acc.z, x.z);
+    acc.w = fmaf(c, acc.w, x.w);
+  }
+  s_in[idx] = acc;
+}
+
+__global__ void prefix_combine_kernel_scalar(const float* __restrict__ gathered, float* __restrict__ s_in,
+                                             SegLens lens, int rank, const float* __restrict__ log2g,
+                                             int H, int64_t per_head, int64_t per_rank) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= per_rank) return;
+  const int h = (int)((idx / per_head) % H);
+  const float lg = log2g[h];
+  float acc = 0.f;
+  for (int p = 0; p < rank; ++p) acc = fmaf(gpow(lg, lens.len[p]), acc, gathered[(int64_t)p * per_rank + idx]);
+  s_in[idx] = acc;
+}
+
+}  // namespace
+
+cudaError_t launch_prefix_combine(const float* gathered, float* s_in, const int64_t* seg_lens,
+                                  int P, int rank, const float* log2g, const ShapeArgs& s,
+                                  cudaStream_t stream) {
+  if (P > MAXP || rank < 0 || rank >= P) return cudaErrorInvalidValue;
+  SegLens lens{};
+  for (int p = 0; p < P; ++p) lens.len[p] = (float)seg_lens[p];
+  const int64_t per_head = s.dk * s.dv;
+  const int64_t per_rank = s.B * s.H * per_head;
+  const bool vec = (per_head % 4 == 0) && ((reinterpret_cast<uintptr_t>(gathered) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(s_in) & 15) == 0);
+  constexpr int NT = 256;
+  if (vec) {
+    const int64_t n4 = per_rank / 4;
+    prefix_combine_kernel<<<(unsigned)((n4 + NT - 1) / NT), NT, 0, stream>>>(
+        (const float4*)gathered, (float4*)s_in, lens, rank, log2g, (int)s.H, per_head / 4, n4);
+  } else {
+    prefix_combine_kernel_scalar<<<(unsigned)((per_rank + NT - 1) / NT), NT, 0, stream>>>(
+        gathered, s_in, lens, rank, log2g, (int)s.H, per_head, per_rank);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace linattn

@@ -1,0 +1,193 @@
+"""Method registry and ``run_method``: the drop-in boundary at run_method level.
+
+The reference routes every method through ``run_method(method, inputs,
+params, validate) -> (out, opcount)`` (kernels.py:257-281), looping over
+(batch, head) slices.  This module keeps that signature and return contract
+but each method here is ONE device launch over the whole (B, H, N, .) tensor:
+
+=====================  =====================================================
+``b200-chunked``       tcgen05 tensor-core chunked prefill, bf16 operands,
+                       fp32 accumulation (replaces block-based /
+                       two-level-block, kernels.py:109-166); tolerance 2e-2
+``b200-chunked-f32``   the same algebra on the fp32 FFMA pipe (parity mode,
+                       tolerance 1e-4 against the f64 oracle)
+``b200-recurrent``     per-token recurrence through the decode-step kernel
+                       (row-based semantics, kernels.py:93-106)
+``b200-seqpar``        two-phase sequence-split prefill (state pass, prefix
+                       combine, seeded prefill) over ``params.seq_parts``
+                       segments on one device (recursion cross term,
+                       kernels.py:185-189); the multi-GPU form is ``sp.py``
+=====================  =====================================================
+
+Output dtype equals input dtype; host (numpy) inputs are staged through the
+device and returned as numpy, device (torch CUDA) inputs stay on the device.
+There is no CPU fallback: without the CUDA library every method raises.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .errors import UsageError
+from .tensor import AttnInputs, validate_inputs
+
+DEFAULT_MEM_CAP = 2 << 30  # kept for signature parity with the reference (oracle.py:16)
+TC_CHUNK = 64      # token chunk of the tensor-core kernel
+SIMT_CHUNK = 32    # token chunk of the fp32 FFMA kernel
+
+REFERENCE_ONLY = ("vanilla", "row-based", "block-based", "recursion", "two-level-block",
+                  "fleet", "fleet-tiled")
+
+
+class MethodId(enum.Enum):
+    B200_CHUNKED = "b200-chunked"
+    B200_CHUNKED_F32 = "b200-chunked-f32"
+    B200_RECURRENT = "b200-recurrent"
+    B200_SEQPAR = "b200-seqpar"
+    AUTO = "auto"
+
+    @classmethod
+    def parse(cls, name: str) -> "MethodId":
+        """String -> MethodId, with the reference's UsageError on unknown names (kernels.py:35-41)."""
+        for m in cls:
+            if m.value == name:
+                return m
+        known = ", ".join(m.value for m in cls)
+        if name in REFERENCE_ONLY:
+            raise UsageError(f"method {name!r} is a CPU route of the reference package; "
+                             f"this package provides the device methods ({known})")
+        raise UsageError(f"unknown method {name!r} (known: {known})")
+
+
+CONCRETE_METHODS = [m for m in MethodId if m is not MethodId.AUTO]
+
+
+@dataclass
+class BlockParams:
+    """Tuning knobs (reference kernels.py:47-61 plus ``seq_parts``).
+
+    ``block_size``/``row_block``/``col_block``/``term_size``/``mem_cap`` are
+    accepted for signature parity; the device kernels use their native chunk
+    (TC_CHUNK / SIMT_CHUNK), which is what the reported opcount assumes.
+    Results are block-size invariant up to the dtype tolerance, as the
+    reference's are (test_kernels.py:114-124).  ``seq_parts`` is the number of
+    sequence segments for ``b200-seqpar``.
+    """
+
+    block_size: int = 64
+    row_block: int = 64
+    col_block: int | None = None
+    term_size: int = 32
+    mem_cap: int = DEFAULT_MEM_CAP
+    seq_parts: int = 2
+
+
+_COMPUTE = {
+    MethodId.B200_CHUNKED: torch.bfloat16,
+    MethodId.B200_CHUNKED_F32: torch.float32,
+    MethodId.B200_RECURRENT: torch.float32,
+    MethodId.B200_SEQPAR: torch.bfloat16,
+}
+
+
+def _to_device(x, dtype):
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda:
+            return x.to(dtype=dtype).contiguous()
+        # host torch tensor: async H2D when pinned, then cast on the device
+        return x.to(device="cuda", non_blocking=x.is_pinned()).to(dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x)).to(device="cuda").to(dtype=dtype)
+
+
+def _seqpar(q, k, v, log2g, parts: int, kernel: str):
+    """Two-phase split on one device; the 'all-gather' is a stack of segment states."""
+    n = q.shape[2]
+    bounds = np.linspace(0, n, parts + 1).astype(int)
+    lens = [int(bounds[p + 1] - bounds[p]) for p in range(parts)]
+    segs = [(int(bounds[p]), int(bounds[p + 1])) for p in range(parts) if lens[p] > 0]
+    lens = [hi - lo for lo, hi in segs]
+    states = torch.stack([ops.state_pass(k[:, :, lo:hi].contiguous(), v[:, :, lo:hi].contiguous(),
+                                         log2g, kernel=kernel) for lo, hi in segs])
+    out = torch.empty_like(v)
+    for p, (lo, hi) in enumerate(segs):
+        s_in = ops.prefix_combine(states, lens, p, log2g) if p > 0 else None
+        out[:, :, lo:hi] = ops.prefill(q[:, :, lo:hi].contiguous(), k[:, :, lo:hi].contiguous(),
+                                       v[:, :, lo:hi].contiguous(), log2g, s_in=s_in, kernel=kernel)
+    return out
+
+
+def _recurrent(q, k, v, log2g):
+    B, H, N, dk = q.shape
+    dv = v.shape[3]
+    state = torch.zeros((B, H, dk, dv), dtype=torch.float32, device=q.device)
+    out = torch.empty_like(v)
+    for i in range(N):
+        out[:, :, i] = ops.decode_step(q[:, :, i].contiguous(), k[:, :, i].contiguous(),
+                                       v[:, :, i].contiguous(), state, log2g)
+    return out
+
+
+def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None = None,
+               validate: bool = True, out=None):
+    """Run a concrete device method; returns (output, analytic opcount) (kernels.py:257-281).
+
+    ``out`` (optional, not in the reference signature) is a caller-owned result
+    buffer of the input's shape and dtype -- e.g. a pinned host tensor, so the
+    device->host copy of a host-tensor call runs at full PCIe bandwidth.
+    """
+    if isinstance(method, str):
+        method = MethodId.parse(method)
+    if method is MethodId.AUTO:
+        raise UsageError("auto must be resolved by dispatch.decode, not run_method")
+    if params is None:
+        params = BlockParams()
+    if validate:
+        validate_inputs(inputs)
+    cdt = _COMPUTE[method]
+    host = not inputs.on_device
+    torch_host = inputs.on_device and not inputs.v.is_cuda
+    in_dtype = inputs.v.dtype
+    q = _to_device(inputs.b, cdt)
+    k = _to_device(inputs.c, cdt)
+    v = _to_device(inputs.v, cdt)
+    log2g = ops.log2_gamma(inputs.gamma, inputs.decay, device=q.device)
+    if method is MethodId.B200_CHUNKED:
+        out_dev = ops.prefill(q, k, v, log2g, kernel="auto")
+        chunk = TC_CHUNK
+    elif method is MethodId.B200_CHUNKED_F32:
+        out_dev = ops.prefill(q, k, v, log2g, kernel="simt")
+        chunk = SIMT_CHUNK
+    elif method is MethodId.B200_SEQPAR:
+        out_dev = _seqpar(q, k, v, log2g, max(1, int(params.seq_parts)), "auto")
+        chunk = TC_CHUNK
+    else:
+        out_dev = _recurrent(q, k, v, log2g)
+        chunk = 1
+    ops_count = ops.chunked_opcount(inputs.batch, inputs.heads, inputs.seqlen, inputs.rank,
+                                    inputs.dim, inputs.decay, chunk)
+    if method is MethodId.B200_RECURRENT:
+        ops_count = inputs.batch * inputs.heads * inputs.seqlen * inputs.rank * inputs.dim * (
+            3 if inputs.decay else 2)  # reference row-based count (kernels.py:105)
+    result = out
+    if host:
+        res = out_dev.float().cpu().numpy().astype(in_dtype, copy=False)
+        if result is not None:
+            result[...] = res
+            return result, ops_count
+        return res, ops_count
+    out = out_dev
+    if torch_host:
+        if result is None:
+            return out.to(in_dtype).cpu(), ops_count
+        result.copy_(out.to(in_dtype), non_blocking=result.is_pinned())
+        torch.cuda.current_stream().synchronize()
+        return result, ops_count
+    if result is not None:
+        result.copy_(out)
+        return result, ops_count
+    return out.to(in_dtype), ops_count

@@ -1,0 +1,161 @@
+"""Device-level operators over torch CUDA tensors (thin wrappers of the C ABI).
+
+These are the hot-path entry points used by ``run_method``, the decode API,
+the sequence-parallel driver and the benchmark.  They validate only what the
+C side cannot see (device, contiguity, dtype agreement); shape checks happen
+in C (include/linattn_b200.h) and surface as the reference exception classes.
+Every call is asynchronous on torch's current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import LinAttnError, ShapeError, UsageError
+
+_DTYPES = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}
+_KERNELS = {"auto": _lib.KERNEL_AUTO, "tc": _lib.KERNEL_TC, "simt": _lib.KERNEL_SIMT}
+
+
+def _require_cuda(*ts):
+    if not torch.cuda.is_available():
+        raise LinAttnError("no CUDA device: the B200 path has no CPU fallback")
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise UsageError("tensor is not on a CUDA device")
+        if not t.is_contiguous():
+            raise UsageError("tensor must be contiguous")
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DTYPES[t.dtype]
+    except KeyError:
+        raise UsageError(f"unsupported device dtype {t.dtype} (expected float32 or bfloat16)")
+
+
+def _ptr(t):
+    return None if t is None else ctypes_ptr(t)
+
+
+def ctypes_ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def log2_gamma(gammas, decay: bool = True, device=None) -> torch.Tensor:
+    """fp32 log2(gamma) per head, computed in f64 ("decay numerics").
+
+    -inf for gamma == 0 (so gamma^n == 0 for n > 0 while gamma^0 stays 1), 0 for
+    gamma == 1 and for the binary mask (decay=False; the reference ignores gamma
+    then, e.g. kernels.py:101).
+    """
+    g = np.asarray(gammas, dtype=np.float64).reshape(-1)
+    if decay:
+        with np.errstate(divide="ignore"):
+            l2 = np.log2(g)
+    else:
+        l2 = np.zeros_like(g)
+    t = torch.from_numpy(l2.astype(np.float32))
+    return t.to(device) if device is not None else t
+
+
+def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "auto"):
+    """O = (Q K^T (.) M_gamma) V on device; optional initial/end state (fp32)."""
+    _require_cuda(q, k, v, log2g, s_in, s_out, out)
+    if not (q.dtype == k.dtype == v.dtype):
+        raise UsageError(f"dtype mismatch: q={q.dtype} k={k.dtype} v={v.dtype}")
+    if q.dim() != 4 or k.shape != q.shape or v.dim() != 4 or v.shape[:3] != q.shape[:3]:
+        raise ShapeError(f"expected q,k [B,H,N,dk] and v [B,H,N,dv]; got {tuple(q.shape)}, "
+                         f"{tuple(k.shape)}, {tuple(v.shape)}")
+    B, H, N, dk = q.shape
+    dv = v.shape[3]
+    if out is None:
+        out = torch.empty_like(v)
+    for st in (s_in, s_out):
+        if st is not None and (st.dtype != torch.float32 or tuple(st.shape) != (B, H, dk, dv)):
+            raise ShapeError(f"state must be float32 [B,H,dk,dv]={B, H, dk, dv}, got {tuple(st.shape)}")
+    lib = _lib.load()
+    _lib.check(lib.linattn_prefill(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                   log2g.data_ptr(), _ptr(s_in), _ptr(s_out), B, H, N, dk, dv,
+                                   _dtype_code(q), _KERNELS[kernel], _stream()))
+    return out
+
+
+def state_pass(k, v, log2g, *, s_out=None, kernel: str = "auto"):
+    """End state sum_t gamma^(N-1-t) k_t^T v_t of each (b, h) segment (fp32)."""
+    _require_cuda(k, v, log2g, s_out)
+    B, H, N, dk = k.shape
+    dv = v.shape[3]
+    if s_out is None:
+        s_out = torch.empty((B, H, dk, dv), dtype=torch.float32, device=k.device)
+    lib = _lib.load()
+    _lib.check(lib.linattn_state_pass(k.data_ptr(), v.data_ptr(), s_out.data_ptr(), log2g.data_ptr(),
+                                      B, H, N, dk, dv, _dtype_code(k), _KERNELS[kernel], _stream()))
+    return s_out
+
+
+def prefix_combine(gathered, seg_lens, rank: int, log2g, *, s_in=None):
+    """Exclusive gamma-weighted prefix of gathered [P,B,H,dk,dv] end states."""
+    _require_cuda(gathered, log2g, s_in)
+    P, B, H, dk, dv = gathered.shape
+    if s_in is None:
+        s_in = torch.empty((B, H, dk, dv), dtype=torch.float32, device=gathered.device)
+    lens = (ctypes.c_int64 * P)(*[int(x) for x in seg_lens])
+    lib = _lib.load()
+    _lib.check(lib.linattn_prefix_combine(gathered.data_ptr(), s_in.data_ptr(), lens, P, rank,
+                                          log2g.data_ptr(), B, H, dk, dv, _stream()))
+    return s_in
+
+
+def decode_step(q, k, v, state, log2g, *, out=None):
+    """S <- gamma S + k^T v ; o = q S for single tokens q,k [B,H,dk], v [B,H,dv]."""
+    _require_cuda(q, k, v, state, log2g, out)
+    if state.dtype != torch.float32:
+        raise UsageError("decode state must be float32")
+    B, H, dk = q.shape[0], q.shape[1], q.shape[-1]
+    dv = v.shape[-1]
+    if tuple(state.shape) != (B, H, dk, dv):
+        raise ShapeError(f"state must be [B,H,dk,dv]={B, H, dk, dv}, got {tuple(state.shape)}")
+    if out is None:
+        out = torch.empty_like(v)
+    lib = _lib.load()
+    _lib.check(lib.linattn_decode_step(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                       state.data_ptr(), log2g.data_ptr(), B, H, dk, dv,
+                                       _dtype_code(q), _stream()))
+    return out
+
+
+def prefill_kernel_name(dk: int, dv: int, dtype=torch.bfloat16, kernel: str = "auto") -> str:
+    """Which kernel family a prefill of this shape runs ("prefill_tc" or "prefill_simt")."""
+    if kernel == "simt":
+        return "prefill_simt"
+    code = _lib.load().linattn_prefill_kernel(dk, dv, _DTYPES[dtype])
+    return "prefill_tc" if code == _lib.KERNEL_TC else "prefill_simt"
+
+
+def chunked_opcount(batch: int, heads: int, n: int, r: int, d: int, decay: bool, chunk: int) -> int:
+    """Analytic two-level-block multiply-add count at chunk ``chunk`` (kernels.py:158-159, 164)."""
+    total = 0
+    full, rem = divmod(n, chunk)
+    for length, count in ((chunk, full), (rem, 1 if rem else 0)):
+        if decay:
+            per = length * length * (r + d + 1) + 2 * length * r + 2 * length * r * d + r * d
+        else:
+            per = length * length * (r + d) + 2 * length * r * d
+        total += per * count
+    return total * batch * heads
+
+
+def bytes_per_token_head(dk: int, dv: int, elem: int = 2) -> int:
+    """Algorithmic prefill bytes per (token, head): q, k, v read once, o written once."""
+    return elem * (2 * dk + 2 * dv)

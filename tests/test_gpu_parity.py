@@ -1,0 +1,254 @@
+"""Device parity: every device method against the oracle / golden vectors.
+
+Tolerances (north star; max-norm relative error, verify.py:22-24):
+  * bf16 tensor-core path ("b200-chunked", "b200-seqpar"): <= 2e-2
+  * fp32 parity mode ("b200-chunked-f32", "b200-recurrent"): <= 1e-4 vs the f64 oracle
+All calls go through the C ABI (liblinattn_b200.so) via the package API.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from la_helpers import FIXTURES, fixture_case
+from oracle import linattn_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+TOL_F32 = 1e-4
+
+
+@pytest.fixture(scope="module")
+def la():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_02573_b200 as la
+    from paper_2501_02573_b200 import _lib
+    _lib.load()  # fail loudly if the library is missing
+    return la
+
+
+def dev(x, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+
+
+def test_library_loaded_and_launches(la):
+    from paper_2501_02573_b200 import _lib
+    before = _lib.launch_count()
+    inp = la.make_inputs(dev(np.ones((4, 2))), dev(np.ones((4, 2))), dev(np.ones((4, 3))))
+    la.run_method(la.MethodId.B200_CHUNKED_F32, inp)
+    torch.cuda.synchronize()
+    assert _lib.launch_count() > before
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("method", ["b200-chunked-f32", "b200-chunked", "b200-recurrent", "b200-seqpar"])
+def test_canonical_fixtures(la, golden, name, method):
+    b, c, v, gamma, decay, expected = fixture_case(golden, name)
+    inp = la.make_inputs(b, c, v, gamma=gamma, decay=decay)   # host f64 arrays, like the reference
+    out, ops = la.run_method(la.MethodId.parse(method), inp)
+    assert isinstance(out, np.ndarray) and out.dtype == np.float64 and ops > 0
+    tol = TOL_BF16 if method in ("b200-chunked", "b200-seqpar") else TOL_F32
+    if name in ("ex_a", "ex_b", "ex_c"):
+        np.testing.assert_allclose(out[0, 0], expected, atol=1e-6)   # exact in bf16 and fp32
+    else:
+        assert orc.max_rel_error(out[0, 0], expected) <= tol
+
+
+def _grid(golden, i):
+    bt, hd, n, r, d, g, decay, bits = golden[f"grid_{i}_cfg"]
+    dtype = np.float64 if int(bits) == 64 else np.float32
+    b, c, v = orc.gen_inputs(int(bt), int(hd), int(n), int(r), int(d), dtype, 2026)
+    return b, c, v, [float(g)] * int(hd), bool(decay)
+
+
+def test_reference_grid_f32_mode(la, golden):
+    worst = 0.0
+    for i in range(int(golden["grid_count"])):
+        b, c, v, gamma, decay = _grid(golden, i)
+        out, _ = la.run_method(la.MethodId.B200_CHUNKED_F32, la.make_inputs(b, c, v, gamma, decay))
+        err = orc.max_rel_error(out, golden[f"grid_{i}_oracle"])
+        worst = max(worst, err)
+        assert err <= TOL_F32, (i, err)
+    print(f"f32 grid worst {worst:.2e}")
+
+
+def test_reference_grid_bf16_tc(la, golden):
+    for i in range(int(golden["grid_count"])):
+        b, c, v, gamma, decay = _grid(golden, i)
+        bq, cq, vq = (dev(orc.bf16_round(x), torch.bfloat16) for x in (b, c, v))
+        inp = la.make_inputs(bq, cq, vq, gamma, decay)
+        out, _ = la.run_method(la.MethodId.B200_CHUNKED, inp)
+        ref = orc.oracle_attn(orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v), gamma, decay)
+        assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16, i
+
+
+@pytest.mark.parametrize("kernel", ["auto", "simt"])
+def test_bf16_golden_cases(la, golden, kernel):
+    from paper_2501_02573_b200 import ops
+    for i in range(int(golden["bf_count"])):
+        bt, hd, n, r, d = (int(x) for x in golden[f"bf_{i}_cfg"])
+        b, c, v = (orc.bf16_round(x) for x in orc.gen_inputs(bt, hd, n, r, d, np.float32, 7))
+        gam = list(golden[f"bf_{i}_gamma"])
+        ref = golden[f"bf_{i}_oracle"]
+        l2 = ops.log2_gamma(gam, True, "cuda")
+        out = ops.prefill(dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16), l2,
+                          kernel=kernel)
+        assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16, (i, kernel)
+        out32 = ops.prefill(dev(b), dev(c), dev(v), l2, kernel="simt")
+        assert orc.max_rel_error(out32.cpu().numpy(), ref) <= TOL_F32, i
+
+
+@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 127, 129, 300])
+@pytest.mark.parametrize("dk,dv", [(64, 64), (128, 128), (32, 48), (256, 128), (128, 256)])
+def test_shapes_and_ragged(la, n, dk, dv):
+    from paper_2501_02573_b200 import ops
+    b, c, v = orc.gen_inputs(2, 3, n, dk, dv, np.float32, 5)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    gam = [0.0, 0.9, 1.0]
+    ref = orc.oracle_attn(b, c, v, gam, True)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    out = ops.prefill(dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16), l2)
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
+    out32 = ops.prefill(dev(b), dev(c), dev(v), l2, kernel="simt")
+    assert orc.max_rel_error(out32.cpu().numpy(), ref) <= TOL_F32
+
+
+def test_binary_mask_and_per_head_gamma(la, golden):
+    inp = la.make_inputs(golden["ph_b"], golden["ph_c"], golden["ph_v"], list(golden["ph_gamma"]), True)
+    out, _ = la.run_method(la.MethodId.B200_CHUNKED_F32, inp)
+    assert orc.max_rel_error(out, golden["ph_oracle"]) <= TOL_F32
+    b, c, v = orc.gen_inputs(1, 2, 150, 16, 8, np.float64, 1)
+    out, _ = la.run_method(la.MethodId.B200_CHUNKED_F32, la.make_inputs(b, c, v, [0.3, 0.5], decay=False))
+    assert orc.max_rel_error(out, orc.oracle_attn(b, c, v, [1.0, 1.0], False)) <= TOL_F32
+
+
+def test_state_out_and_state_pass(la):
+    from paper_2501_02573_b200 import ops
+    b, c, v = orc.gen_inputs(2, 2, 200, 64, 64, np.float32, 8)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    gam = [0.95, 1.0]
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    ref = np.stack([[orc.segment_end_state(c[x, h], v[x, h], gam[h]) for h in range(2)] for x in range(2)])
+    for kernel in ("auto", "simt"):
+        for dt in (torch.bfloat16, torch.float32):
+            s = ops.state_pass(dev(c, dt), dev(v, dt), l2, kernel=kernel if dt == torch.bfloat16 else "simt")
+            assert orc.max_rel_error(s.cpu().numpy(), ref) <= 1e-5
+            s_out = torch.empty_like(s)
+            ops.prefill(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_out=s_out,
+                        kernel=kernel if dt == torch.bfloat16 else "simt")
+            assert orc.max_rel_error(s_out.cpu().numpy(), ref) <= 1e-5
+
+
+def test_prefix_combine(la):
+    from paper_2501_02573_b200 import ops
+    rng = np.random.default_rng(0)
+    P, B, H, dk, dv = 5, 2, 3, 8, 12
+    states = rng.standard_normal((P, B, H, dk, dv)).astype(np.float32)
+    lens = [7, 0, 130, 1, 64]
+    gam = [0.0, 0.97, 1.0]
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    for rank in range(P):
+        got = ops.prefix_combine(dev(states), lens, rank, l2).cpu().numpy()
+        for h in range(H):
+            want = orc.exclusive_prefix_states([states[p][:, h] for p in range(P)], lens, gam[h])[rank]
+            np.testing.assert_allclose(got[:, h], want, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 4])
+def test_seqpar_loopback(la, parts):
+    b, c, v = orc.gen_inputs(1, 4, 1000, 128, 128, np.float32, 12)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    gam = [1 - 2.0 ** -5, 1 - 2.0 ** -10, 1 - 2.0 ** -15, 0.5]
+    inp = la.make_inputs(dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16), gam, True)
+    out, _ = la.run_method(la.MethodId.B200_SEQPAR, inp, la.BlockParams(seq_parts=parts))
+    assert orc.max_rel_error(out.float().cpu().numpy(), orc.oracle_attn(b, c, v, gam, True)) <= TOL_BF16
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+def test_prefill_then_decode_continuity(la, dt):
+    b, c, v = orc.gen_inputs(2, 3, 300, 64, 128, np.float32, 13)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    gam = [0.0, 0.97, 1.0]
+    ref = orc.oracle_attn(b, c, v, gam, True)
+    pre = la.make_inputs(dev(b[:, :, :256], dt), dev(c[:, :, :256], dt), dev(v[:, :, :256], dt), gam, True)
+    out, state = la.prefill_with_state(pre, kernel="simt" if dt == torch.float32 else "auto")
+    tol = TOL_F32 if dt == torch.float32 else TOL_BF16
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref[:, :, :256]) <= tol
+    outs = [state.step(dev(b[:, :, i], dt), dev(c[:, :, i], dt), dev(v[:, :, i], dt)) for i in range(256, 300)]
+    got = torch.stack(outs, dim=2).float().cpu().numpy()
+    assert orc.max_rel_error(got, ref[:, :, 256:]) <= tol
+
+
+def test_decode_steps_vs_oracle(la):
+    from paper_2501_02573_b200 import ops
+    rng = np.random.default_rng(3)
+    B, H, dk, dv, T = 4, 3, 128, 128, 20
+    s0 = rng.standard_normal((B, H, dk, dv))
+    q, k, v = (rng.standard_normal((B, H, T, d)) for d in (dk, dk, dv))
+    gam = [0.0, 0.9, 1.0]
+    ref, ref_s = orc.decode_steps(q, k, v, s0, gam)
+    st = dev(s0)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    outs = [ops.decode_step(dev(q[:, :, i]), dev(k[:, :, i]), dev(v[:, :, i]), st, l2) for i in range(T)]
+    got = torch.stack(outs, 2).cpu().numpy()
+    assert orc.max_rel_error(got, ref) <= TOL_F32
+    assert orc.max_rel_error(st.cpu().numpy(), ref_s) <= TOL_F32
+
+
+@pytest.mark.parametrize("dk,dv", [(3, 5), (64, 62), (128, 512)])
+def test_decode_odd_shapes(la, dk, dv):
+    from paper_2501_02573_b200 import ops
+    rng = np.random.default_rng(4)
+    B, H = 2, 2
+    s0 = rng.standard_normal((B, H, dk, dv))
+    q, k, v = (rng.standard_normal((B, H, 1, d)) for d in (dk, dk, dv))
+    ref, ref_s = orc.decode_steps(q, k, v, s0, [0.8, 1.0])
+    st = dev(s0)
+    o = ops.decode_step(dev(q[:, :, 0]), dev(k[:, :, 0]), dev(v[:, :, 0]), st,
+                        ops.log2_gamma([0.8, 1.0], True, "cuda"))
+    assert orc.max_rel_error(o.cpu().numpy(), ref[:, :, 0]) <= TOL_F32
+    assert orc.max_rel_error(st.cpu().numpy(), ref_s) <= TOL_F32
+
+
+def test_full_size_properties(la):
+    """cfg2-shaped (B=8,H=32,N=8192,d=128) properties the oracle cannot check densely."""
+    from paper_2501_02573_b200 import ops
+    torch.manual_seed(0)
+    B, H, N, d = 8, 32, 8192, 128
+    q = torch.randn(B, H, N, d, device="cuda", dtype=torch.bfloat16)
+    k = torch.randn_like(q)
+    v = torch.randn_like(q)
+    gam = [1 - 2.0 ** (-5 - 10 * h / (H - 1)) for h in range(H)]
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    o = ops.prefill(q, k, v, l2)
+    # linearity in V: scaling by 2 is exact in bf16 and fp32
+    o2 = ops.prefill(q, k, (2 * v).contiguous(), l2)
+    assert torch.equal(o2, 2 * o)
+    # causality: perturbing the last 1000 tokens leaves the first 7168 outputs bitwise unchanged
+    k2 = k.clone()
+    k2[:, :, 7192:] = torch.randn_like(k2[:, :, 7192:])
+    o3 = ops.prefill(q, k2, v, l2)
+    assert torch.equal(o3[:, :, :7168], o[:, :, :7168])
+    # sampled slices against the f64 oracle
+    for (bi, h) in [(0, 0), (7, 31)]:
+        ref = orc.oracle_attn(q[bi:bi + 1, h:h + 1].float().cpu().numpy(), k[bi:bi + 1, h:h + 1].float().cpu().numpy(),
+                              v[bi:bi + 1, h:h + 1].float().cpu().numpy(), [gam[h]], True)
+        assert orc.max_rel_error(o[bi, h].float().cpu().numpy(), ref[0, 0]) <= TOL_BF16
+    # sequence split on one device agrees with the single pass (two-phase, 4 segments)
+    inp = la.make_inputs(q[:1], k[:1], v[:1], gam, True)
+    sp, _ = la.run_method(la.MethodId.B200_SEQPAR, inp, la.BlockParams(seq_parts=4))
+    assert orc.max_rel_error(sp.float().cpu().numpy(), o[:1].float().cpu().numpy()) <= TOL_BF16
+
+
+def test_cfg3_shape_small_n(la):
+    """RetNet-shaped heads: dk=256, dv=512 (configs[2]) at a size the oracle can check."""
+    from paper_2501_02573_b200 import ops
+    b, c, v = orc.gen_inputs(1, 2, 257, 256, 512, np.float32, 14)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    gam = [1 - 2.0 ** -5, 1 - 2.0 ** -8]
+    ref = orc.oracle_attn(b, c, v, gam, True)
+    out = ops.prefill(dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16),
+                      ops.log2_gamma(gam, True, "cuda"))
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
