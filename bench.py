@@ -265,7 +265,8 @@ def run_ours(args):
     # decode step (configs[3]): 1024 single-token steps, state 256x32x128x128 fp32 (512 MiB)
     dec = None
     if not args.no_decode:
-        DB, DH, ddk, ddv, T = DEC["B"], DEC["H"], DEC["dk"], DEC["dv"], DEC["steps"]
+        DB, DH, ddk, ddv = DEC["B"], DEC["H"], DEC["dk"], DEC["dv"]
+        T = max(64, args.decode_steps // 64 * 64)
         state = torch.zeros(DB, DH, ddk, ddv, device=dev, dtype=torch.float32)
         qd = torch.randn(DB, DH, ddk, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
         kd = torch.randn(DB, DH, ddk, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
@@ -296,7 +297,7 @@ def run_ours(args):
         us = max_over_ranks(d0.elapsed_time(d1) * 1e3 / T)
         dbytes = DB * DH * (2 * 4 * ddk * ddv + 2 * (2 * ddk + 2 * ddv))
         gbs = dbytes / (us * 1e-6) / 1e9
-        dec = {"workload": "configs[3] decode step B=256,H=32,d=128, fp32 state, bf16 q/k/v/o, 1024 steps "
+        dec = {"workload": f"configs[3] decode step B=256,H=32,d=128, fp32 state, bf16 q/k/v/o, {T} steps "
                            "(CUDA graph of 64 steps)",
                "us_per_step": us, "hbm_gbs": gbs, "frac_of_hbm": gbs / hbm,
                "bytes_per_step": dbytes, "steps": T}
@@ -350,6 +351,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--decode-steps", type=int, default=DEC["steps"],
+                    help="decode steps timed for the configs[3] sub-benchmark (multiple of 64)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

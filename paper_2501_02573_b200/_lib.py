@@ -11,7 +11,8 @@ import os
 
 from .errors import LinAttnError, ParameterError, ShapeError, UsageError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "liblinattn_b200.so")
+LIB_PATH = os.environ.get("LINATTN_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "liblinattn_b200.so")  # LINATTN_LIB: dev A/B builds
 
 OK, ESHAPE, EPARAM, EDTYPE, EUNSUPPORTED, ECUDA = range(6)
 F32, BF16 = 0, 1

@@ -125,6 +125,10 @@ int linattn_prefill_kernel(int64_t dk, int64_t dv, int dtype) {
   return tc_supported(s, dtype) ? LINATTN_KERNEL_TC : LINATTN_KERNEL_SIMT;
 }
 
+// Debug hook (not part of the public header): record per-chunk clock64 timestamps of
+// CTA (0,0) of subsequent tensor-core launches into a device buffer of 16 x 4096 u64.
+__attribute__((visibility("default"))) void linattn_debug_set_trace(void* dev_buf) { set_trace(dev_buf); }
+
 const char* linattn_last_error(void) { return g_last_error.c_str(); }
 
 int linattn_abi_version(void) { return LINATTN_ABI_VERSION; }

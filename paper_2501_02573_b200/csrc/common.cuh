@@ -49,6 +49,7 @@ cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void*
                               const float* log2g, const float* s_in, float* s_out,
                               const ShapeArgs& s, bool state_only, cudaStream_t stream);
 bool tc_supported(const ShapeArgs& s, int dtype);
+void set_trace(void* buf);  // debug only: per-chunk clock64 trace of CTA (0,0), nullptr = off
 
 cudaError_t launch_decode_step(const void* q, const void* k, const void* v, void* o,
                                float* state, const float* log2g, const ShapeArgs& s,

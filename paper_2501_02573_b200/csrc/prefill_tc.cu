@@ -1,13 +1,893 @@
-// K1: tensor-core chunked prefill (tcgen05 + TMA).  Placeholder until the kernel lands.
+// K1 (+K2, K4): tensor-core chunked prefill for sm_100a -- TMA + tcgen05 + TMEM.
+//
+// One CTA owns one (batch*head, 128-wide dv tile) unit and walks its sequence in
+// chunks of C = 64 tokens.  The algebra is the reference two-level-block method
+// (kernels.py:139-166) written TRANSPOSED so every accumulator has M = 128 TMEM
+// lanes (lane = dv row) and the chunk can stay at the reference's C = 64:
+//
+//   MMA1  P^T[s][t]   = sum_i K[s][i] Q[t][i]              (M=128 (64 live), N=64, K=dk)
+//   epi1  P^T[s][t]  *= gamma^(t-s) for t >= s else 0      (mask built from a gamma^n table)
+//         K'[s]       = gamma^(L-1-s) K[s]                 (in place, smem)
+//   MMA2  Oi^T[d][t]  = sum_s V[s][d] P^T[s][t]             (M=128, N=64, K=64)
+//         Ox^T[d][t]  = sum_i S^T[d][i] Q[t][i]             (M=128, N=64, K=dk)
+//         S^T[d][i]  += sum_s V[s][d] K'[s][i]              (M=128, N=dk, K=64)
+//   epi2  O[t][d]     = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t]
+//         S^T (fp32, TMEM) -> bf16 smem operand for the next chunk, then S^T *= gamma^L_next
+//
+// Warp roles (320 threads): warps 0-3 epilogue-1 (P^T mask on lanes 0-63, K' scaling),
+// warps 4-7 epilogue-2 (outputs and state), warp 8 TMA producer, warp 9 MMA issuer
+// and TMEM owner.  Q/K/V chunks stream through an mbarrier ring of STAGES slots;
+// all operands are bf16 in 128B-swizzled shared memory; accumulators are fp32 in TMEM.
+#include <mutex>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace linattn {
+namespace {
 
-bool tc_supported(const ShapeArgs&, int) { return false; }
+using namespace sm100;
 
-cudaError_t launch_prefill_tc(const void*, const void*, const void*, void*, const float*,
-                              const float*, float*, const ShapeArgs&, bool, cudaStream_t) {
-  return cudaErrorNotSupported;
+constexpr int kC = 64;          // tokens per chunk
+constexpr int kDVT = 128;       // dv rows per CTA (MMA M)
+constexpr int kThreads = 320;
+constexpr uint32_t kTmemCols = 512;
+// TMEM column map
+constexpr uint32_t T_PT = 0, T_OI = 64, T_OX = 128, T_S = 256;
+
+template <int DK, int STAGES>
+struct Cfg {
+  static constexpr int KB = DK / 64;
+  static constexpr int Q_BYTES = kC * DK * 2;
+  static constexpr int K_BYTES = kC * DK * 2;
+  static constexpr int V_BYTES = kC * kDVT * 2;
+  static constexpr int STAGE_BYTES = Q_BYTES + K_BYTES + V_BYTES;
+  static constexpr int OFF_PT = STAGES * STAGE_BYTES;
+  static constexpr int PT_BYTES = kC * kC * 2;
+  static constexpr int OFF_ST = OFF_PT + PT_BYTES;
+  static constexpr int ST_BYTES = kDVT * DK * 2;
+  static constexpr int OFF_POW = OFF_ST + ST_BYTES;
+  static constexpr int OFF_BAR = OFF_POW + 128 * 4;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;  // barriers + TMEM slot + alignment slack
+};
+
+__device__ __forceinline__ uint4 scale_bf16x8(uint4 x, float w) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(&x);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float lo = __uint_as_float(u[i] << 16) * w;
+    const float hi = __uint_as_float(u[i] & 0xFFFF0000u) * w;
+    u[i] = pack_bf16x2(lo, hi);
+  }
+  return x;
+}
+
+// Write 32 fp32 values (columns col0..col0+31 of row `row`) as bf16 into a K-major
+// SW128 operand whose 64-column blocks are `block_bytes` apart.
+__device__ __forceinline__ void store_row_bf16_sw128(uint8_t* base, int block_bytes, int row,
+                                                     int col0, const float (&v)[32]) {
+  uint8_t* blk = base + (col0 / 64) * block_bytes + row * 128;
+  const int c0 = (col0 % 64) / 8;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 pk;
+    pk.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+    pk.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+    pk.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+    pk.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+    *reinterpret_cast<uint4*>(blk + (((c0 + j) ^ (row & 7)) << 4)) = pk;
+  }
+}
+
+template <int DK, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
+                  const float* __restrict__ log2g, const float* __restrict__ s_in,
+                  float* __restrict__ s_out, int H, int N, int dv, int state_only,
+                  unsigned long long* __restrict__ trace) {
+  using G = Cfg<DK, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* empty = full + STAGES;
+  uint64_t* mma1_bar = empty + STAGES;
+  uint64_t* epi1_bar = mma1_bar + 1;
+  uint64_t* mma2_bar = epi1_bar + 1;
+  uint64_t* epi2_bar = mma2_bar + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi2_bar + 1);
+  float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);  // pw[n] = gamma^n, n = 0..64
+  uint8_t* pt_smem = smem + G::OFF_PT;
+  uint8_t* st_smem = smem + G::OFF_ST;
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int bh = blockIdx.y;
+  const int j0 = blockIdx.x * kDVT;
+  const int nchunks = (N + kC - 1) / kC;
+  const float lg = log2g[bh % H];
+
+  if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
+  if (warp == 8 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(mma1_bar, 1);
+    mbar_init(epi1_bar, state_only ? 64 : 128);  // state pass: only the K' warps arrive
+    mbar_init(mma2_bar, 1);
+    mbar_init(epi2_bar, 128);
+    fence_barrier_init();
+    if (!state_only) tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+  }
+  if (warp == 9) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  // optional per-chunk timestamps of CTA (0, 0) for pipeline analysis (trace[event * 4096 + chunk])
+  const bool tracing = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
+#define LA_TRACE(ev, c) \
+  do { if (tracing && (c) < 4096) trace[(ev) * 4096 + (c)] = clock64(); } while (0)
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES + G::V_BYTES;
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % STAGES;
+        const int use = c / STAGES;
+        mbar_wait(&empty[s], (use & 1) ^ 1);
+        uint8_t* st = smem + s * G::STAGE_BYTES;
+        LA_TRACE(0, c);
+        mbar_arrive_expect_tx(&full[s], bytes);
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb) {
+          if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, c * kC, bh);
+          tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, c * kC, bh);
+        }
+#pragma unroll
+        for (int nb = 0; nb < kDVT / 64; ++nb)
+          tma_load_3d(st + G::Q_BYTES + G::K_BYTES + nb * 8192, &tm_v, &full[s], j0 + nb * 64,
+                      c * kC, bh);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id_qk = idesc_bf16(128, kC, false, false);   // P^T = K Q^T
+      constexpr uint32_t id_vp = idesc_bf16(128, kC, true, true);     // Oi^T = V^T P^T
+      constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // Ox^T = S^T Q^T
+      constexpr uint32_t id_vk = idesc_bf16(128, DK, true, true);     // S^T += V^T K'
+      const uint32_t pt_addr = smem_u32(pt_smem);
+      const uint32_t st_addr = smem_u32(st_smem);
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % STAGES;
+        const int use = c / STAGES;
+        mbar_wait(&full[s], use & 1);
+        LA_TRACE(1, c);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(smem + s * G::STAGE_BYTES);
+        const uint32_t k_addr = q_addr + G::Q_BYTES;
+        const uint32_t v_addr = k_addr + G::K_BYTES;
+        if (!state_only) {
+#pragma unroll
+          for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss(tbase + T_PT, smem_desc_sw128(k_addr + kb * 8192 + kk * 32, 16, 1024),
+                          smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_qk,
+                          (kb | kk) != 0);
+          mma_commit(mma1_bar);
+        }
+        mbar_wait(epi1_bar, c & 1);
+        LA_TRACE(2, c);
+        mbar_wait(epi2_bar, c & 1);
+        LA_TRACE(3, c);
+        tc_fence_after();
+        if (!state_only) {
+#pragma unroll
+          for (int ks = 0; ks < kC / 16; ++ks)
+            mma_bf16_ss(tbase + T_OI, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
+                        smem_desc_sw128(pt_addr + ks * 2048, 8192, 1024), id_vp, ks != 0);
+#pragma unroll
+          for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss(tbase + T_OX, smem_desc_sw128(st_addr + kb * (kDVT * 128) + kk * 32, 16, 1024),
+                          smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq,
+                          (kb | kk) != 0);
+        }
+#pragma unroll
+        for (int ks = 0; ks < kC / 16; ++ks)
+          mma_bf16_ss(tbase + T_S, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
+                      smem_desc_sw128(k_addr + ks * 2048, 8192, 1024), id_vk, 1);
+        mma_commit(mma2_bar);
+        mma_commit(&empty[s]);
+      }
+    }
+  } else if (warp < 4) {
+    // ------------------------------------------------------------ epilogue 1
+    // (in the state pass the P^T warps have no work and must not arrive: an mbarrier
+    //  cannot tell arrivals of different chunks apart, so idle warps would lap)
+    for (int c = 0; c < (state_only && warp < 2 ? 0 : nchunks); ++c) {
+      const int s = c % STAGES;
+      const int use = c / STAGES;
+      const int L = min(kC, N - c * kC);
+      mbar_wait(&full[s], use & 1);
+      // MMA1 reads K unscaled: both the P^T warps and the K' warps wait for it
+      if (!state_only) {
+        mbar_wait(mma1_bar, c & 1);
+        tc_fence_after();
+      }
+      if (threadIdx.x == 0) LA_TRACE(4, c);
+      uint8_t* k_smem = smem + s * G::STAGE_BYTES + G::Q_BYTES;
+      if (warp < 2) {
+        if (!state_only) {
+          const int srow = warp * 32 + lane;
+          const uint32_t ta = tbase + ((warp * 32) << 16) + T_PT;
+          float p0[32], p1[32];
+          tmem_ld32(ta, p0);
+          tmem_ld32(ta + 32, p1);
+          tmem_wait_ld();
+          uint8_t* row = pt_smem + srow * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float m[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int t = 8 * j + e;
+              const float pv = t < 32 ? p0[t] : p1[t - 32];
+              m[e] = t >= srow ? pv * pw[(t - srow) & 63] : 0.f;
+            }
+            uint4 pk;
+            pk.x = pack_bf16x2(m[0], m[1]);
+            pk.y = pack_bf16x2(m[2], m[3]);
+            pk.z = pack_bf16x2(m[4], m[5]);
+            pk.w = pack_bf16x2(m[6], m[7]);
+            *reinterpret_cast<uint4*>(row + ((j ^ (srow & 7)) << 4)) = pk;
+          }
+        }
+      } else {
+        const int srow = (warp - 2) * 32 + lane;
+        const float w = srow < L ? pw[L - 1 - srow] : 0.f;
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb) {
+          uint8_t* row = k_smem + kb * 8192 + srow * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint4* p = reinterpret_cast<uint4*>(row + ((j ^ (srow & 7)) << 4));
+            *p = scale_bf16x8(*p, w);
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      if (threadIdx.x == 0 || threadIdx.x == 64) LA_TRACE(threadIdx.x == 0 ? 5 : 6, c);
+      mbar_arrive(epi1_bar);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue 2
+    const int sub = warp - 4;                 // TMEM subpartition of this warp
+    const int d = sub * 32 + lane;            // dv row within the tile
+    const int jd = j0 + d;
+    const bool dv_ok = jd < dv;
+    const uint32_t ta = tbase + ((sub * 32) << 16);
+    {
+      const float carry = pw[min(kC, N)];
+      for (int cb = 0; cb < DK / 32; ++cb) {
+        float sv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          sv[i] = (s_in && dv_ok) ? s_in[((size_t)bh * DK + cb * 32 + i) * dv + jd] : 0.f;
+        store_row_bf16_sw128(st_smem, kDVT * 128, d, cb * 32, sv);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[i] *= carry;
+        tmem_st32(ta + T_S + cb * 32, sv);
+      }
+      tmem_wait_st();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(epi2_bar);
+    }
+    for (int c = 0; c < nchunks; ++c) {
+      const int L = min(kC, N - c * kC);
+      const bool last = c == nchunks - 1;
+      mbar_wait(mma2_bar, c & 1);
+      if (threadIdx.x == 128) LA_TRACE(7, c);
+      tc_fence_after();
+      if (!state_only) {
+        __nv_bfloat16* orow = o + ((size_t)bh * N + (size_t)c * kC) * dv + jd;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float a[32], b[32];
+          tmem_ld32(ta + T_OI + half * 32, a);
+          tmem_ld32(ta + T_OX + half * 32, b);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int t = half * 32 + i;
+            if (t < L && dv_ok) orow[(size_t)t * dv] = __float2bfloat16_rn(fmaf(pw[t + 1], b[i], a[i]));
+          }
+        }
+      }
+      const float carry = last ? 0.f : pw[min(kC, N - (c + 1) * kC)];
+      for (int cb = 0; cb < DK / 32; ++cb) {
+        float sv[32];
+        tmem_ld32(ta + T_S + cb * 32, sv);
+        tmem_wait_ld();
+        if (last) {
+          if (s_out && dv_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) s_out[((size_t)bh * DK + cb * 32 + i) * dv + jd] = sv[i];
+          }
+        } else {
+          store_row_bf16_sw128(st_smem, kDVT * 128, d, cb * 32, sv);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[i] *= carry;
+          tmem_st32(ta + T_S + cb * 32, sv);
+        }
+      }
+      if (threadIdx.x == 128) LA_TRACE(8, c);
+      if (!last) {
+        tmem_wait_st();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        if (threadIdx.x == 128) LA_TRACE(9, c);
+        mbar_arrive(epi2_bar);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 9) tmem_dealloc<kTmemCols>(tbase);
+}
+
+// ============================================================================================
+// Pipelined variant for dk <= 128 (the configs[1] hot path).  Same algebra, organised so the
+// per-chunk serial chain is short and every epilogue is a few instructions per element:
+//   * the running state S lives in REGISTERS of 8 state warps (fp32); the tensor pipe only
+//     produces dS_c = V^T K'_c into a TMEM scratch, so the state update never round-trips
+//     through TMEM and never blocks the next chunk's MMAs;
+//   * P^T and both output accumulators (Oi = V^T P^T, Ox = S^T Q^T) are double-buffered in
+//     TMEM (P^T x2, Oi x2, Ox x2, dS = 512 columns) and MMA1 of chunk c+1 runs ahead;
+//   * decay masks are applied as packed bf16x2 multiplies from a (gamma^k, gamma^(k+1)) table
+//     (P^T and K'); the inter-chunk weight gamma^(t+1) is applied exactly in fp32 when the
+//     output tile is combined;
+//   * outputs leave through tcgen05.ld.16x256b -> stmatrix.trans -> TMA bulk store.
+// Per-chunk critical chain: publish S_c -> {O_c, dS_c} MMAs -> state warps load dS_c ->
+// publish S_{c+1}.
+// Warp roles (448 threads): 0-1 P^T mask, 2-3 K' scaling, 4-11 state + outputs,
+// 12 TMA producer, 13 MMA issuer / TMEM owner.
+namespace v2 {
+
+constexpr int kThreads = 448;
+#ifndef LA_L2_AHEAD
+#define LA_L2_AHEAD 0
+#endif
+constexpr int kL2Ahead = LA_L2_AHEAD;   // chunks of L2 prefetch beyond the smem ring
+// TMEM column map: P^T x2 | O x2 | dS | S^T (bf16 A operand) x2
+constexpr uint32_t T_P = 0, T_O = 128, T_DS = 256, T_ST = 384;
+
+template <int DK, int STAGES>
+struct Cfg {
+  static constexpr int KB = DK / 64;
+  static constexpr int Q_BYTES = kC * DK * 2;
+  static constexpr int K_BYTES = kC * DK * 2;
+  static constexpr int V_BYTES = kC * kDVT * 2;
+  static constexpr int STAGE_BYTES = Q_BYTES + K_BYTES + V_BYTES;
+  static constexpr int PT_BYTES = kC * kC * 2;
+  static constexpr int OT_BYTES = kC * kDVT * 2;    // one output staging tile [64 t][128 d]
+  static constexpr int OFF_PT = STAGES * STAGE_BYTES;
+  static constexpr int OFF_OT = OFF_PT + 2 * PT_BYTES;
+  static constexpr int OFF_POW = OFF_OT + OT_BYTES;           // fp32 gamma^n, n = 0..64
+  static constexpr int OFF_POW2 = OFF_POW + 128 * 4;          // bf16x2 (gamma^k, gamma^(k+1)), k = -64..127
+  static constexpr int OFF_BAR = OFF_POW2 + 192 * 4;
+  static constexpr int SMEM = OFF_BAR + 512 + 1024;
+};
+
+__device__ __forceinline__ uint32_t hmul2_bf16(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+template <int DK, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                       const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                       const float* __restrict__ log2g, const float* __restrict__ s_in,
+                       float* __restrict__ s_out, int H, int N, int dv, int state_only,
+                       unsigned long long* __restrict__ trace) {
+  using G = Cfg<DK, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* empty = full + STAGES;
+  uint64_t* mma1_bar = empty + STAGES;   // [2] P^T accumulator b ready
+  uint64_t* epi1_bar = mma1_bar + 2;     // [2] P^T smem b written, K' scaled     (64 or 128 arrivals)
+  uint64_t* mma_s_bar = epi1_bar + 2;    // dS_c ready
+  uint64_t* ds_free = mma_s_bar + 1;     // dS read by the state warps            (256 arrivals)
+  uint64_t* st_full = ds_free + 1;       // [2] S^T bf16 operand b published (TMEM) (256 arrivals)
+  uint64_t* mma_o_bar = st_full + 2;     // [2] O accumulator b ready
+  uint64_t* o_free = mma_o_bar + 2;      // [2] O accumulators b drained          (256 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+  float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);
+  uint32_t* pw2 = reinterpret_cast<uint32_t*>(smem + G::OFF_POW2) + 64;   // pw2[k], k in [-64, 127]
+  uint8_t* pt_smem = smem + G::OFF_PT;
+  uint8_t* ot_smem = smem + G::OFF_OT;
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int bh = blockIdx.y;
+  const int j0 = blockIdx.x * kDVT;
+  const int nchunks = (N + kC - 1) / kC;
+  const float lg = log2g[bh % H];
+
+  if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
+  if (threadIdx.x < 192) {
+    const int k = (int)threadIdx.x - 64;
+    const float lo = k >= 0 ? gpow(lg, (float)k) : 0.f;
+    const float hi = k + 1 >= 0 ? gpow(lg, (float)(k + 1)) : 0.f;
+    pw2[k] = pack_bf16x2(lo, hi);
+  }
+  if (warp == 12 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&mma1_bar[b], 1);
+      mbar_init(&epi1_bar[b], state_only ? 64 : 128);
+      mbar_init(&o_free[b], 256);
+      mbar_init(&mma_o_bar[b], 1);
+    }
+    mbar_init(mma_s_bar, 1);
+    mbar_init(ds_free, 256);
+    mbar_init(&st_full[0], 256);
+    mbar_init(&st_full[1], 256);
+    fence_barrier_init();
+    if (!state_only) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_o);
+    }
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+  }
+  if (warp == 13) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const bool tracing = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
+  const int lin_block = blockIdx.y * gridDim.x + blockIdx.x;
+  auto gtime = [] {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (trace != nullptr && threadIdx.x == 0 && lin_block < 4096) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    trace[8 * 4096 + lin_block] = gtime();
+    trace[0 * 4096 + lin_block] = smid;
+  }
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ P^T mask / K' scaling
+    for (int c = 0; c < (state_only && warp < 2 ? 0 : nchunks); ++c) {
+      const int s = c % STAGES;
+      const int b = c & 1;
+      const int L = min(kC, N - c * kC);
+      mbar_wait(&full[s], (c / STAGES) & 1);
+      if (!state_only) {
+        mbar_wait(&mma1_bar[b], (c >> 1) & 1);      // MMA1 has consumed the unscaled K
+        tc_fence_after();
+      }
+      if (warp < 2) {
+        // P^T[s][t] *= gamma^(t-s) (t >= s), bf16: row s of the MN-major B operand of Oi
+        const int srow = warp * 32 + lane;
+        const uint32_t ta = tbase + ((warp * 32) << 16) + T_P + b * kC;
+        uint8_t* row = pt_smem + b * G::PT_BYTES + srow * 128;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float p[32];
+          tmem_ld32(ta + half * 32, p);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int t0 = half * 32 + 8 * j;
+            uint4 pk;
+            pk.x = hmul2_bf16(pack_bf16x2(p[8 * j + 0], p[8 * j + 1]), pw2[t0 + 0 - srow]);
+            pk.y = hmul2_bf16(pack_bf16x2(p[8 * j + 2], p[8 * j + 3]), pw2[t0 + 2 - srow]);
+            pk.z = hmul2_bf16(pack_bf16x2(p[8 * j + 4], p[8 * j + 5]), pw2[t0 + 4 - srow]);
+            pk.w = hmul2_bf16(pack_bf16x2(p[8 * j + 6], p[8 * j + 7]), pw2[t0 + 6 - srow]);
+            *reinterpret_cast<uint4*>(row + (((half * 4 + j) ^ (srow & 7)) << 4)) = pk;
+          }
+        }
+        // Q'[t] = gamma^(t+1) Q[t] in place (rows >= L are TMA zero-fill and never stored)
+        const uint32_t w2 = pw2[srow + 1];
+        const uint32_t wq = (w2 & 0xFFFFu) | (w2 << 16);
+        uint8_t* q_smem = smem + s * G::STAGE_BYTES;
+        uint4 x[G::KB * 8];
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            x[kb * 8 + j] = *reinterpret_cast<const uint4*>(q_smem + kb * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4));
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint4 y = x[kb * 8 + j];
+            y.x = hmul2_bf16(y.x, wq);
+            y.y = hmul2_bf16(y.y, wq);
+            y.z = hmul2_bf16(y.z, wq);
+            y.w = hmul2_bf16(y.w, wq);
+            *reinterpret_cast<uint4*>(q_smem + kb * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4)) = y;
+          }
+      } else {
+        // K'[s] = gamma^(L-1-s) K[s], zero beyond the ragged end (in place, bf16x2 multiplies)
+        const int srow = (warp - 2) * 32 + lane;
+        const uint32_t w2 = pw2[srow < L ? L - 1 - srow : -64];     // pw2[-64] = (0, 0)
+        const uint32_t wk = (w2 & 0xFFFFu) | (w2 << 16);
+        uint8_t* k_smem = smem + s * G::STAGE_BYTES + G::Q_BYTES;
+        uint4 x[G::KB * 8];                       // issue every load before the first store
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            x[kb * 8 + j] = *reinterpret_cast<const uint4*>(k_smem + kb * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4));
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint4 y = x[kb * 8 + j];
+            y.x = hmul2_bf16(y.x, wk);
+            y.y = hmul2_bf16(y.y, wk);
+            y.z = hmul2_bf16(y.z, wk);
+            y.w = hmul2_bf16(y.w, wk);
+            *reinterpret_cast<uint4*>(k_smem + kb * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4)) = y;
+          }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      if (tracing && lane == 0) trace[(warp < 2 ? 3 : 4) * 4096 + c] = clock64();
+      mbar_arrive(&epi1_bar[b]);
+    }
+  } else if (warp < 12) {
+    // ------------------------------------------------------------ running state + outputs
+    // warp (g, sub): TMEM lanes sub*32.. (dv rows d); state columns [g*SC, (g+1)*SC);
+    // output rows d0 = sub*32 + g*16 .. +15 (a 16-lane half of the subpartition).
+    constexpr int SC = DK / 2;
+    const int g = (warp - 4) / 4;
+    const int sub = (warp - 4) % 4;
+    const int d = sub * 32 + lane;
+    const int jd = j0 + d;
+    const bool dv_ok = jd < dv;
+    const int col0 = g * SC;
+    const uint32_t ta_s = tbase + ((sub * 32) << 16) + T_DS + col0;
+    const int d0 = sub * 32 + g * 16;
+    const uint32_t ta_o = tbase + ((uint32_t)d0 << 16);
+    const bool leader = (warp == 4 && lane == 0);
+    float S[SC];
+#pragma unroll
+    for (int i = 0; i < SC; ++i) S[i] = (s_in && dv_ok) ? s_in[((size_t)bh * DK + col0 + i) * dv + jd] : 0.f;
+    // S (fp32 regs) -> bf16 pairs -> TMEM S^T operand buffer `buf` (row d, columns col0/2..)
+    const uint32_t ta_st = tbase + ((sub * 32) << 16) + T_ST + col0 / 2;
+    auto publish = [&](int buf) {
+#pragma unroll
+      for (int j = 0; j < SC / 32; ++j) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(S[32 * j + 2 * i], S[32 * j + 2 * i + 1]);
+        tmem_st16(ta_st + buf * (DK / 2) + 16 * j, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&st_full[buf]);
+    };
+    if (!state_only) publish(0);
+    // stmatrix row address of this thread: matrix m = lane/8 of each x4 group, row lane%8
+    const int mrow = lane & 7;
+    const int mi = lane >> 3;                  // 0: (d0, t), 1: (d0+8, t), 2: (d0, t+8), 3: (d0+8, t+8)
+    const int md = d0 + (mi & 1) * 8;          // 8-aligned dv row of the tile this address serves
+    for (int c = 0; c < nchunks; ++c) {
+      const int L = min(kC, N - c * kC);
+      const int b = c & 1;
+      mbar_wait(mma_s_bar, c & 1);
+      tc_fence_after();
+      const float carry = pw[L];
+#pragma unroll
+      for (int j = 0; j < SC / 16; ++j) {
+        float ds[16];
+        tmem_ld16(ta_s + 16 * j, ds);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) S[16 * j + i] = fmaf(carry, S[16 * j + i], ds[i]);
+      }
+      tc_fence_before();
+      mbar_arrive(ds_free);
+      if (tracing && lane == 0 && sub == 0 && g == 0) trace[6 * 4096 + c] = clock64();
+      if (c == nchunks - 1) {
+        if (s_out && dv_ok) {
+#pragma unroll
+          for (int i = 0; i < SC; ++i) s_out[((size_t)bh * DK + col0 + i) * dv + jd] = S[i];
+        }
+      }
+      if (state_only) continue;
+      if (c != nchunks - 1) {
+        // buffer (c+1)&1 was last read by Ox_{c-1}, which precedes dS_c in the tensor pipe
+        publish((c + 1) & 1);
+        if (tracing && lane == 0 && sub == 0 && g == 0) trace[7 * 4096 + c] = clock64();
+      }
+      mbar_wait(&mma_o_bar[b], (c >> 1) & 1);    // O_c done
+      tc_fence_after();
+      // ---- outputs of chunk c: O = Oi + gamma^(t+1) Ox (16 lanes x 64 tokens) -> bf16 ->
+      //      smem [t][d] (stmatrix.trans, 128B swizzle) -> TMA bulk store (clips N and dv)
+      uint8_t* ot = ot_smem;
+      if (leader) bulk_wait_read<0>();           // the previous chunk's store has read the tile
+      named_bar_sync(1, 256);
+#pragma unroll
+      for (int q4 = 0; q4 < 2; ++q4) {           // tokens q4*32 .. q4*32+31
+        uint32_t ro[16];
+        tmem_ld_16x256b_x4(ta_o + T_O + b * kC + q4 * 32, ro);
+        tmem_wait_ld();
+        if (q4 == 1) {
+          tc_fence_before();
+          mbar_arrive(&o_free[b]);
+        }
+        uint32_t pk[8];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {            // 8-token group r: t = q4*32 + 8r + tq + {0,1}
+          pk[2 * r + 0] = pack_bf16x2(__uint_as_float(ro[4 * r + 0]), __uint_as_float(ro[4 * r + 1]));
+          pk[2 * r + 1] = pack_bf16x2(__uint_as_float(ro[4 * r + 2]), __uint_as_float(ro[4 * r + 3]));
+        }
+#pragma unroll
+        for (int rr = 0; rr < 4; rr += 2) {      // two 8-token groups per stmatrix.x4
+          const int tt = q4 * 32 + rr * 8 + (mi >> 1) * 8 + mrow;     // token row this lane addresses
+          const uint32_t addr = smem_u32(ot + (md / 64) * (kC * 128) + tt * 128 +
+                                         ((((md % 64) >> 3) ^ (tt & 7)) << 4));
+          stmatrix_x4_trans(addr, pk[2 * rr + 0], pk[2 * rr + 1], pk[2 * rr + 2], pk[2 * rr + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(2, 256);
+      if (leader) {
+        tma_store_3d(&tm_o, ot, j0, c * kC, bh);
+        tma_store_3d(&tm_o, ot + kC * 128, j0 + 64, c * kC, bh);
+        bulk_commit();
+      }
+      if (tracing && lane == 0 && sub == 0 && g == 0) trace[5 * 4096 + c] = clock64();
+    }
+    if (leader) bulk_wait<0>();
+  } else {
+    if (warp == 12) {
+      // ---------------------------------------------------------- TMA producer
+      if (lane == 0) {
+        const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES + G::V_BYTES;
+        for (int c = 0; c < nchunks; ++c) {
+          const int s = c % STAGES;
+          mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
+          if (tracing) trace[13 * 4096 + c] = clock64();
+          uint8_t* st = smem + s * G::STAGE_BYTES;
+          if (kL2Ahead > 0 && c == 0) {  // warm L2 with the first chunks too
+            for (int cp = 1; cp < STAGES + kL2Ahead && cp < nchunks; ++cp) {
+              for (int kb = 0; kb < G::KB; ++kb) {
+                if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, cp * kC, bh);
+                tma_prefetch_l2_3d(&tm_k, kb * 64, cp * kC, bh);
+              }
+              for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, cp * kC, bh);
+            }
+          }
+          mbar_arrive_expect_tx(&full[s], bytes);
+          if (kL2Ahead > 0 && c + STAGES + kL2Ahead < nchunks) {  // keep HBM requests ahead of the smem ring
+            const int cp = c + STAGES + kL2Ahead;
+            for (int kb = 0; kb < G::KB; ++kb) {
+              if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, cp * kC, bh);
+              tma_prefetch_l2_3d(&tm_k, kb * 64, cp * kC, bh);
+            }
+            for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, cp * kC, bh);
+          }
+#pragma unroll
+          for (int kb = 0; kb < G::KB; ++kb) {
+            if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, c * kC, bh);
+            tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, c * kC, bh);
+          }
+#pragma unroll
+          for (int nb = 0; nb < kDVT / 64; ++nb)
+            tma_load_3d(st + G::Q_BYTES + G::K_BYTES + nb * 8192, &tm_v, &full[s], j0 + nb * 64,
+                        c * kC, bh);
+        }
+      }
+    } else if (warp == 13) {
+      // ---------------------------------------------------------- MMA issuer (whole warp)
+      constexpr uint32_t id_qk = idesc_bf16(128, kC, false, false);   // P^T = K Q^T
+      constexpr uint32_t id_vp = idesc_bf16(128, kC, true, true);     // O^T  = V^T P^T
+      constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // O^T += S^T(TMEM) Q'^T
+      constexpr uint32_t id_vk = idesc_bf16(128, DK, true, true);     // dS^T = V^T K'
+      const uint32_t base_addr = smem_u32(smem);
+      const uint32_t pt_addr = smem_u32(pt_smem);
+      auto issue_mma1 = [&](int c) {
+        const int s = c % STAGES;
+        mbar_wait(&full[s], (c / STAGES) & 1);
+        if (tracing && lane == 0) trace[10 * 4096 + c] = clock64();
+        tc_fence_after();
+        const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
+        const uint32_t k_addr = q_addr + G::Q_BYTES;
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16_ss_elect(tbase + T_P + (c & 1) * kC, smem_desc_sw128(k_addr + kb * 8192 + kk * 32, 16, 1024),
+                              smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_qk, (kb | kk) != 0);
+        mma_commit_elect(&mma1_bar[c & 1]);
+        if (tracing && lane == 0) trace[11 * 4096 + c] = clock64();
+      };
+      if (!state_only) issue_mma1(0);
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % STAGES;
+        const int b = c & 1;
+        const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
+        const uint32_t k_addr = q_addr + G::Q_BYTES;
+        const uint32_t v_addr = k_addr + G::K_BYTES;
+        if (!state_only) {
+          if (c + 1 < nchunks) issue_mma1(c + 1);      // run ahead into the other P^T buffer
+        } else {
+          mbar_wait(&full[s], (c / STAGES) & 1);
+        }
+        mbar_wait(&epi1_bar[b], (c >> 1) & 1);         // P^T_c in smem, K'_c scaled
+        if (tracing && lane == 0) trace[12 * 4096 + c] = clock64();
+        if (c > 0) mbar_wait(ds_free, (c - 1) & 1);    // state warps hold dS_{c-1}
+        tc_fence_after();
+        if (tracing && lane == 0) trace[1 * 4096 + c] = clock64();
+#pragma unroll
+        for (int ks = 0; ks < kC / 16; ++ks)
+          mma_bf16_ss_elect(tbase + T_DS, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
+                            smem_desc_sw128(k_addr + ks * 2048, 8192, 1024), id_vk, ks != 0);
+        mma_commit_elect(mma_s_bar);
+        if (!state_only) {
+          mbar_wait(&st_full[b], (c >> 1) & 1);        // S_c (bf16) published in TMEM buffer b
+          if (tracing && lane == 0) trace[14 * 4096 + c] = clock64();
+          if (c >= 2) mbar_wait(&o_free[b], ((c >> 1) - 1) & 1);
+          tc_fence_after();
+          if (tracing && lane == 0) trace[2 * 4096 + c] = clock64();
+#pragma unroll
+          for (int ks = 0; ks < kC / 16; ++ks)
+            mma_bf16_ss_elect(tbase + T_O + b * kC, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
+                              smem_desc_sw128(pt_addr + b * G::PT_BYTES + ks * 2048, 8192, 1024), id_vp, ks != 0);
+#pragma unroll
+          for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ts_elect(tbase + T_O + b * kC, tbase + T_ST + b * (DK / 2) + (kb * 4 + kk) * 8,
+                                smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq, 1);
+          mma_commit_elect(&mma_o_bar[b]);
+        }
+        mma_commit_elect(&empty[s]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (trace != nullptr && threadIdx.x == 0 && lin_block < 4096) trace[9 * 4096 + lin_block] = gtime();
+  if (warp == 13) tmem_dealloc<kTmemCols>(tbase);
+}
+
+}  // namespace v2
+
+// ---- host side ---------------------------------------------------------------------------
+
+unsigned long long* g_trace = nullptr;  // debug: set by linattn_debug_set_trace
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// [BH][N][D] bf16 viewed as a 3-D tensor (D fastest); 64 x 64 boxes, 128B swizzle.
+bool make_map(CUtensorMap* map, const void* base, int64_t D, int64_t N, int64_t BH) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)N, (cuuint64_t)BH};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)(N * D * 2)};
+  cuuint32_t box[3] = {64, 64, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int DK, int STAGES>
+cudaError_t launch_dk(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                      const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
+                      cudaStream_t stream) {
+  using G = Cfg<DK, STAGES>;
+  static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
+  CUtensorMap mq, mk, mv;
+  const int64_t BH = s.B * s.H;
+  if (!make_map(&mk, k, s.dk, s.N, BH) || !make_map(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
+  if (state_only) {
+    mq = mk;
+  } else if (!make_map(&mq, q, s.dk, s.N, BH)) {
+    return cudaErrorInvalidValue;
+  }
+  auto kern = prefill_tc_kernel<DK, STAGES>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  if (err != cudaSuccess) return err;
+  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH);
+  kern<<<grid, kThreads, G::SMEM, stream>>>(mq, mk, mv, (__nv_bfloat16*)o, log2g, s_in, s_out,
+                                            (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
+                                            g_trace);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int DK, int STAGES>
+cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                        const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
+                        cudaStream_t stream) {
+  using G = v2::Cfg<DK, STAGES>;
+  static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
+  CUtensorMap mq, mk, mv;
+  const int64_t BH = s.B * s.H;
+  if (!make_map(&mk, k, s.dk, s.N, BH) || !make_map(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
+  if (state_only) {
+    mq = mk;
+  } else if (!make_map(&mq, q, s.dk, s.N, BH)) {
+    return cudaErrorInvalidValue;
+  }
+  CUtensorMap mo = mk;
+  if (!state_only && !make_map(&mo, o, s.dv, s.N, BH)) return cudaErrorInvalidValue;
+  auto kern = v2::prefill_tc_pipe_kernel<DK, STAGES>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  if (err != cudaSuccess) return err;
+  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH);
+  kern<<<grid, v2::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out,
+                                                (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
+                                                g_trace);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+void set_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
+
+bool tc_supported(const ShapeArgs& s, int dtype) {
+  if (dtype != LINATTN_BF16) return false;
+  if (!(s.dk == 64 || s.dk == 128 || s.dk == 256)) return false;
+  if (s.dv % 64 != 0) return false;
+  return encode_fn() != nullptr;
+}
+
+cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void* o,
+                              const float* log2g, const float* s_in, float* s_out,
+                              const ShapeArgs& s, bool state_only, cudaStream_t stream) {
+  for (const void* p : {q, k, v, (const void*)o})
+    if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return cudaErrorNotSupported;
+  switch (s.dk) {
+    case 64: return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, state_only, stream);
+    case 128: return launch_pipe<128, 4>(q, k, v, o, log2g, s_in, s_out, s, state_only, stream);
+    case 256: return launch_dk<256, 1>(q, k, v, o, log2g, s_in, s_out, s, state_only, stream);
+    default: return cudaErrorNotSupported;
+  }
 }
 
 }  // namespace linattn
