@@ -141,12 +141,11 @@ class ClockSampler:
         h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
         self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         while not self._stop.is_set():
-            self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
             mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            for name, bit in self.REASONS.items():
-                if mask & bit:
-                    self.reasons.add(name)
-            self._stop.wait(0.005)
+            self.samples.append((time.perf_counter(), mhz, mask))
+            self._ready.set()
+            self._stop.wait(0.002)
 
     def __enter__(self):
         import threading
@@ -156,9 +155,14 @@ class ClockSampler:
         except Exception:  # no NVML: report no samples rather than fail the bench
             return self
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._thread = threading.Thread(target=self._run, daemon=True)
         self._thread.start()
+        self._ready.wait(2.0)
         return self
+
+    def mark(self, which):
+        setattr(self, "t_" + which, time.perf_counter())
 
     def __exit__(self, *exc):
         if self._stop is not None:
@@ -166,9 +170,12 @@ class ClockSampler:
             self._thread.join()
 
     def summary(self):
-        sm = self.samples
+        t0, t1 = getattr(self, "t_start", None), getattr(self, "t_end", None)
+        inside = [s for s in self.samples if t0 is not None and t0 <= s[0] <= t1] or self.samples
+        sm = [s[1] for s in inside]
+        reasons = sorted({n for s in inside for n, bit in self.REASONS.items() if s[2] & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml, 5 ms"}
+                "reasons": reasons, "samples": len(sm), "source": "nvml, 2 ms, inside the timed region"}
 
 
 def load_profile_traffic(kernel_key):
@@ -230,11 +237,13 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
+        clk.mark("start")
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark("end")
         barrier()
     launches = _lib.launch_count() - launches0
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
@@ -310,7 +319,7 @@ def run_ours(args):
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
         with mproc.get_context("spawn").Pool(cores) as pool:
             cpu_sample(pool, cores)
-            cv, cdt, slices = cpu_sample(pool, cores, per_core=2, seed=77)
+            cv, cdt, slices = cpu_sample(pool, cores, per_core=8, seed=77)
         cpu = {"value": cv, "unit": "tokens/s", "cores": cores, "kind": "port",
                "sample": f"{slices} of {B * H} (b,h) slices of configs[1], f32 two-level-block chunk {C0} "
                          f"(oracle/linattn_oracle.py), process pool x{cores}, {cdt:.1f} s"}
@@ -346,7 +355,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-decode", action="store_true")

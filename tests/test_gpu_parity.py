@@ -133,12 +133,15 @@ def test_state_out_and_state_pass(la):
     ref = np.stack([[orc.segment_end_state(c[x, h], v[x, h], gam[h]) for h in range(2)] for x in range(2)])
     for kernel in ("auto", "simt"):
         for dt in (torch.bfloat16, torch.float32):
-            s = ops.state_pass(dev(c, dt), dev(v, dt), l2, kernel=kernel if dt == torch.bfloat16 else "simt")
-            assert orc.max_rel_error(s.cpu().numpy(), ref) <= 1e-5
+            k_sel = kernel if dt == torch.bfloat16 else "simt"
+            # fp32-FFMA kernel: fp32 everywhere -> 1e-5.  Tensor-core kernel: the decayed keys
+            # K' = gamma^(L-1-s) K are bf16 MMA operands -> bf16-level state error.
+            tol = 2e-3 if ops.prefill_kernel_name(64, 64, dt, k_sel) == "prefill_tc" else 1e-5
+            s = ops.state_pass(dev(c, dt), dev(v, dt), l2, kernel=k_sel)
+            assert orc.max_rel_error(s.cpu().numpy(), ref) <= tol
             s_out = torch.empty_like(s)
-            ops.prefill(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_out=s_out,
-                        kernel=kernel if dt == torch.bfloat16 else "simt")
-            assert orc.max_rel_error(s_out.cpu().numpy(), ref) <= 1e-5
+            ops.prefill(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_out=s_out, kernel=k_sel)
+            assert orc.max_rel_error(s_out.cpu().numpy(), ref) <= tol
 
 
 def test_prefix_combine(la):
