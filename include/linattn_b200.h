@@ -97,6 +97,44 @@ LINATTN_API int linattn_decode_step(const void* q, const void* k, const void* v,
                         const float* log2g, int64_t B, int64_t H, int64_t dk, int64_t dv,
                         int dtype, void* stream);
 
+/* ---- Sequence segments (split inside one device; local half of multi-GPU sequence parallel) ----
+ * Segment p covers tokens [p*seg_len, (p+1)*seg_len) clipped at N; with a sub-split m it is cut
+ * into m sub-segments of sub = roundup(ceil(seg_len/m), 64) tokens, indexed z = p*m + r.
+ * Tensor-core segments must be multiples of 64 tokens (only the last one may be ragged).
+ * The algebra is the reference recursion cross term (kernels.py:185-189) applied across
+ * segments: the state at token lo is gamma^lo*s_in + sum_{z: hi_z <= lo} gamma^(lo-hi_z)*loc[z].
+ * linattn_prefill (AUTO/TC) applies this split itself when B*H*ceil(dv/128) leaves SMs idle,
+ * with a workspace from a library-owned stream-ordered pool. */
+
+/* Plan linattn_prefill would use: plan = {seg_len, nseg, m, sub}; nseg == 1 means no split. */
+LINATTN_API int linattn_seq_plan(int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv, int dtype,
+                                 int kernel, int64_t* plan);
+
+/* Local end states (each from a zero state) of the first nseg segments, m sub-segments each:
+ * loc_out [nseg*m][B][H][dk][dv] fp32 (device).  Replaces, per sub-segment, the decayed carry
+ * u <- gamma^L u + (w_rev c)^T v of the reference blocking routes (kernels.py:125-128). */
+LINATTN_API int linattn_state_pass_segmented(const void* k, const void* v, float* loc_out,
+                                             const float* log2g, int64_t B, int64_t H, int64_t N,
+                                             int64_t dk, int64_t dv, int dtype, int kernel,
+                                             int64_t seg_len, int64_t m, int64_t nseg, void* stream);
+
+/* Prefill with every segment of seg_len tokens running in parallel, each seeded from s_in
+ * (nullable; the state before token 0) and the nloc local states `loc` produced by
+ * linattn_state_pass_segmented with geometry (loc_seg_len, loc_m).  The caller guarantees loc
+ * covers every token before the last segment.  s_out (nullable) receives the end state. */
+LINATTN_API int linattn_prefill_segmented(const void* q, const void* k, const void* v, void* o,
+                                          const float* log2g, const float* s_in, float* s_out,
+                                          const float* loc, int64_t loc_seg_len, int64_t loc_m,
+                                          int64_t nloc, int64_t B, int64_t H, int64_t N, int64_t dk,
+                                          int64_t dv, int dtype, int kernel, int64_t seg_len,
+                                          void* stream);
+
+/* out = gamma^pos * s_in + sum_{z: hi_z <= pos} gamma^(pos - hi_z) * loc[z]   ([B,H,dk,dv] fp32);
+ * with pos == N this is the end state of the whole sequence from its segment-local states. */
+LINATTN_API int linattn_state_at(const float* loc, int64_t loc_seg_len, int64_t loc_m, int64_t nloc,
+                                 const float* s_in, float* out, int64_t pos, const float* log2g,
+                                 int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv, void* stream);
+
 /* Kernel family LINATTN_KERNEL_AUTO resolves to for this shape/dtype (TC or SIMT). */
 LINATTN_API int linattn_prefill_kernel(int64_t dk, int64_t dv, int dtype);
 

@@ -32,6 +32,12 @@ _SIGS = {
                                _i64, _i64, _i64, _i64, _vp],
     "linattn_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp],
     "linattn_prefill_kernel": [_i64, _i64, ctypes.c_int],
+    "linattn_seq_plan": [_i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i64)],
+    "linattn_state_pass_segmented": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int,
+                                     ctypes.c_int, _i64, _i64, _i64, _vp],
+    "linattn_prefill_segmented": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64,
+                                  _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _i64, _vp],
+    "linattn_state_at": [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
     "linattn_last_error": [],
     "linattn_abi_version": [],
     "linattn_launch_count": [],

@@ -1,9 +1,11 @@
 // extern "C" boundary of liblinattn_b200.so (declared in include/linattn_b200.h).
 // Host-side validation mirrors the reference's typed errors (tensor.py:97-123,
 // errors.py:4-29); every entry point is stream-ordered and never synchronises.
+#include <algorithm>
 #include <cstdio>
 #include <cstdarg>
 #include <atomic>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -44,6 +46,96 @@ static int check_dims(const ShapeArgs& s, bool need_n) {
   return LINATTN_OK;
 }
 
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+static int sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// Library-owned stream-ordered pool for split workspaces (never trimmed: no re-mapping per call).
+static cudaMemPool_t work_pool() {
+  static cudaMemPool_t pools[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev] = p;
+  }
+  return pools[dev];
+}
+
+// Sub-segment length of a segment of seg_len tokens split m ways (multiple of the TC chunk).
+static int64_t sub_len(int64_t seg_len, int64_t m) { return m <= 1 ? seg_len : round_up(ceil_div(seg_len, m), 64); }
+
+static SegArgs make_seg(int64_t seg_len, int64_t m) {
+  SegArgs a;
+  a.seg_len = (int)std::min<int64_t>(seg_len, 0x7fffffff);
+  a.m = (int)m;
+  a.sub = (int)std::min<int64_t>(sub_len(seg_len, m), 0x7fffffff);
+  return a;
+}
+
+static void attach_loc(SegArgs& a, const float* loc, int64_t loc_seg_len, int64_t loc_m, int64_t nloc) {
+  a.loc = loc;
+  a.loc_seg_len = (int)loc_seg_len;
+  a.loc_m = (int)loc_m;
+  a.loc_sub = (int)sub_len(loc_seg_len, loc_m);
+  a.nloc = loc ? (int)nloc : 0;
+}
+
+// Sequence-split plan for one device: when batch x head x dv-tiles
+// leaves SMs idle, cut the sequence into nseg segments so nseg * units fills one wave; the
+// state-only pass over the first nseg-1 segments is split m more ways to fill its own wave.
+struct Plan {
+  int64_t seg_len, nseg, m;
+};
+
+static Plan plan_split(const ShapeArgs& s, int dtype, int kernel) {
+  Plan p{s.N, 1, 1};
+  if (kernel == LINATTN_KERNEL_SIMT || !tc_supported(s, dtype)) return p;
+  const int64_t sms = sm_count();
+  const int64_t units = s.B * s.H * ceil_div(s.dv, 128);
+  int64_t nseg = std::min<int64_t>(sms / std::max<int64_t>(units, 1), s.N / 512);
+  if (nseg < 2) return p;
+  const int64_t seg = round_up(ceil_div(s.N, nseg), 64);
+  nseg = ceil_div(s.N, seg);
+  if (nseg < 2) return p;
+  const int64_t ua = units * (nseg - 1);
+  int64_t best_m = 1;
+  double best = 0.0;
+  for (int64_t m = 1; m <= 8; ++m) {
+    if (sub_len(seg, m) < 256) break;
+    const int64_t ctas = ua * m;
+    const double eff = (double)ctas / (double)(ceil_div(ctas, sms) * sms);
+    if (eff > best + 0.02) {
+      best = eff;
+      best_m = m;
+    }
+  }
+  p.seg_len = seg;
+  p.nseg = nseg;
+  p.m = best_m;
+  return p;
+}
+
 static int check_dtype(int dtype) {
   if (dtype != LINATTN_F32 && dtype != LINATTN_BF16)
     return fail(LINATTN_EDTYPE, "unsupported dtype code %d (expected f32=0 or bf16=1)", dtype);
@@ -71,9 +163,32 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
                 "(got dtype=%d dk=%lld dv=%lld)", dtype, (long long)dk, (long long)dv);
   if (kernel != LINATTN_KERNEL_AUTO && kernel != LINATTN_KERNEL_TC && kernel != LINATTN_KERNEL_SIMT)
     return fail(LINATTN_EPARAM, "unknown kernel selector %d", kernel);
-  if (kernel != LINATTN_KERNEL_SIMT && tc_ok)
-    return cuda_status(launch_prefill_tc(q, k, v, o, log2g, s_in, s_out, s, false, st), "prefill_tc");
-  return cuda_status(launch_prefill_simt(q, k, v, o, log2g, s_in, s_out, s, dtype, false, st),
+  if (kernel != LINATTN_KERNEL_SIMT && tc_ok) {
+    const Plan pl = plan_split(s, dtype, kernel);
+    if (pl.nseg > 1) {
+      // two-phase split: local states of segments 0..nseg-2 (m-way sub-split), then every
+      // segment seeded from them in its prologue; workspace from the library's stream pool
+      const int64_t nloc = (pl.nseg - 1) * pl.m;
+      const size_t bytes = (size_t)nloc * s.B * s.H * s.dk * s.dv * sizeof(float);
+      float* loc = nullptr;
+      cudaMemPool_t pool = work_pool();
+      if (pool && cudaMallocFromPoolAsync((void**)&loc, bytes, pool, st) == cudaSuccess) {
+        SegArgs a = make_seg(pl.seg_len, pl.m);
+        cudaError_t e = launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, loc, s, true, a, (int)nloc, st);
+        if (e == cudaSuccess) {
+          SegArgs b = make_seg(pl.seg_len, 1);
+          attach_loc(b, loc, pl.seg_len, pl.m, nloc);
+          e = launch_prefill_tc(q, k, v, o, log2g, s_in, s_out, s, false, b, (int)pl.nseg, st);
+        }
+        cudaFreeAsync(loc, st);
+        return cuda_status(e, "prefill_tc (sequence split)");
+      }
+      cudaGetLastError();  // no workspace: run unsplit
+    }
+    return cuda_status(launch_prefill_tc(q, k, v, o, log2g, s_in, s_out, s, false, SegArgs{}, 1, st),
+                       "prefill_tc");
+  }
+  return cuda_status(launch_prefill_simt(q, k, v, o, log2g, s_in, s_out, s, dtype, false, SegArgs{}, 1, st),
                      "prefill_simt");
 }
 
@@ -89,10 +204,98 @@ int linattn_state_pass(const void* k, const void* v, float* s_out, const float* 
   if (kernel == LINATTN_KERNEL_TC && !tc_ok)
     return fail(LINATTN_EUNSUPPORTED, "tensor-core state pass needs bf16 and a supported shape");
   if (kernel != LINATTN_KERNEL_SIMT && tc_ok)
-    return cuda_status(launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, s_out, s, true, st),
-                       "state_pass_tc");
+    return cuda_status(launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, s_out, s, true,
+                                         SegArgs{}, 1, st), "state_pass_tc");
   return cuda_status(launch_prefill_simt(nullptr, k, v, nullptr, log2g, nullptr, s_out, s, dtype,
-                                         true, st), "state_pass_simt");
+                                         true, SegArgs{}, 1, st), "state_pass_simt");
+}
+
+static int check_seg(const ShapeArgs& s, int64_t seg_len, int64_t m, bool tc) {
+  if (seg_len < 1 || m < 1 || m > 64)
+    return fail(LINATTN_EPARAM, "segment length must be >= 1 and sub-split in [1, 64] (got %lld, %lld)",
+                (long long)seg_len, (long long)m);
+  if (tc && seg_len < s.N && seg_len % 64 != 0)
+    return fail(LINATTN_EPARAM, "tensor-core segments must be multiples of 64 tokens (got %lld)",
+                (long long)seg_len);
+  return LINATTN_OK;
+}
+
+int linattn_seq_plan(int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv, int dtype, int kernel,
+                     int64_t* plan) {
+  ShapeArgs s{B, H, N, dk, dv};
+  if (int e = check_dims(s, true)) return e;
+  if (int e = check_dtype(dtype)) return e;
+  if (!plan) return fail(LINATTN_EPARAM, "null plan pointer");
+  const Plan p = plan_split(s, dtype, kernel);
+  plan[0] = p.seg_len;
+  plan[1] = p.nseg;
+  plan[2] = p.m;
+  plan[3] = sub_len(p.seg_len, p.m);
+  return LINATTN_OK;
+}
+
+int linattn_state_pass_segmented(const void* k, const void* v, float* loc_out, const float* log2g,
+                                 int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv, int dtype,
+                                 int kernel, int64_t seg_len, int64_t m, int64_t nseg, void* stream) {
+  ShapeArgs s{B, H, N, dk, dv};
+  if (int e = check_dims(s, true)) return e;
+  if (int e = check_dtype(dtype)) return e;
+  if (!k || !v || !loc_out || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
+  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype);
+  if (kernel == LINATTN_KERNEL_TC && !tc)
+    return fail(LINATTN_EUNSUPPORTED, "tensor-core state pass needs bf16 and a supported shape");
+  if (int e = check_seg(s, seg_len, m, tc)) return e;
+  if (nseg < 1 || nseg > ceil_div(N, seg_len) || nseg * m > 65535)
+    return fail(LINATTN_EPARAM, "segment count %lld outside [1, ceil(N/seg_len)=%lld]", (long long)nseg,
+                (long long)ceil_div(N, seg_len));
+  const SegArgs a = make_seg(seg_len, m);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tc)
+    return cuda_status(launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, loc_out, s, true, a,
+                                         (int)(nseg * m), st), "state_pass_tc (segmented)");
+  return cuda_status(launch_prefill_simt(nullptr, k, v, nullptr, log2g, nullptr, loc_out, s, dtype, true,
+                                         a, (int)(nseg * m), st), "state_pass_simt (segmented)");
+}
+
+int linattn_prefill_segmented(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                              const float* s_in, float* s_out, const float* loc, int64_t loc_seg_len,
+                              int64_t loc_m, int64_t nloc, int64_t B, int64_t H, int64_t N, int64_t dk,
+                              int64_t dv, int dtype, int kernel, int64_t seg_len, void* stream) {
+  ShapeArgs s{B, H, N, dk, dv};
+  if (int e = check_dims(s, true)) return e;
+  if (int e = check_dtype(dtype)) return e;
+  if (!q || !k || !v || !o || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
+  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype);
+  if (kernel == LINATTN_KERNEL_TC && !tc)
+    return fail(LINATTN_EUNSUPPORTED, "tensor-core prefill needs bf16, dk in {64,128,256}, dv %% 64 == 0");
+  if (int e = check_seg(s, seg_len, 1, tc)) return e;
+  if (loc && (nloc < 0 || loc_seg_len < 1 || loc_m < 1 || nloc > ceil_div(N, loc_seg_len) * loc_m))
+    return fail(LINATTN_EPARAM, "bad local-state geometry (seg_len %lld, m %lld, count %lld)",
+                (long long)loc_seg_len, (long long)loc_m, (long long)nloc);
+  const int64_t nseg = ceil_div(N, seg_len);
+  if (nseg > 65535) return fail(LINATTN_EPARAM, "too many segments (%lld)", (long long)nseg);
+  SegArgs a = make_seg(seg_len, 1);
+  attach_loc(a, loc, loc_seg_len, loc_m, nloc);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tc)
+    return cuda_status(launch_prefill_tc(q, k, v, o, log2g, s_in, s_out, s, false, a, (int)nseg, st),
+                       "prefill_tc (segmented)");
+  return cuda_status(launch_prefill_simt(q, k, v, o, log2g, s_in, s_out, s, dtype, false, a, (int)nseg, st),
+                     "prefill_simt (segmented)");
+}
+
+int linattn_state_at(const float* loc, int64_t loc_seg_len, int64_t loc_m, int64_t nloc, const float* s_in,
+                     float* out, int64_t pos, const float* log2g, int64_t B, int64_t H, int64_t N,
+                     int64_t dk, int64_t dv, void* stream) {
+  ShapeArgs s{B, H, N, dk, dv};
+  if (int e = check_dims(s, true)) return e;
+  if (!out || !log2g || (!loc && nloc > 0)) return fail(LINATTN_EPARAM, "null pointer");
+  if (pos < 0 || pos > N) return fail(LINATTN_EPARAM, "position %lld outside [0, N]", (long long)pos);
+  if (loc && (loc_seg_len < 1 || loc_m < 1 || nloc < 0 || nloc > ceil_div(N, loc_seg_len) * loc_m))
+    return fail(LINATTN_EPARAM, "bad local-state geometry");
+  SegArgs a = make_seg(N, 1);
+  attach_loc(a, loc, loc_seg_len, loc_m, nloc);
+  return cuda_status(launch_state_at(loc, s_in, out, a, pos, log2g, s, (cudaStream_t)stream), "state_at");
 }
 
 int linattn_prefix_combine(const float* gathered, float* s_in, const int64_t* seg_lens, int P,

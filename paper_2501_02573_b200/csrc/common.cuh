@@ -39,15 +39,56 @@ struct ShapeArgs {
   int64_t B, H, N, dk, dv;
 };
 
+// Sequence-segment geometry of one launch (sequence split inside a device, and the local
+// half of multi-GPU sequence parallelism).  blockIdx.z = p * m + r walks segment p
+// (tokens [p*seg_len, (p+1)*seg_len) clipped at N), sub-segment r of `sub` tokens.
+// `loc` optionally holds the LOCAL end states (from a zero state) of the sub-segments of an
+// earlier state-only launch with geometry (loc_seg_len, loc_sub, loc_m); a segment starting
+// at token lo is seeded with
+//     S_init = gamma^lo * s_in + sum_{q : hi_q <= lo} gamma^(lo - hi_q) * loc[q]
+// which is the reference recursion cross term (kernels.py:185-189) applied across segments.
+struct SegArgs {
+  int seg_len = 0x7fffffff, sub = 0x7fffffff, m = 1;
+  const float* loc = nullptr;
+  int loc_seg_len = 0, loc_sub = 0, loc_m = 1, nloc = 0;
+};
+
+__host__ __device__ __forceinline__ void seg_bounds(int seg_len, int sub, int m, int z, int N, int& lo,
+                                                    int& hi) {
+  const int p = z / m, r = z % m;
+  const long long base = (long long)p * seg_len;
+  const long long a = base + (long long)r * sub;
+  const long long b = base + (long long)min((long long)(r + 1) * sub, (long long)seg_len);
+  lo = (int)min(a, (long long)N);
+  hi = (int)min(b, (long long)N);
+}
+
+// Weight of loc entry q for a segment starting at `lo`: gamma^(lo - hi_q) if the entry lies
+// entirely before lo, else 0 (returned as a negative flag).
+__device__ __forceinline__ float seg_loc_weight(const SegArgs& sa, int q, int N, int lo, float lg) {
+  int qlo, qhi;
+  seg_bounds(sa.loc_seg_len, sa.loc_sub, sa.loc_m, q, N, qlo, qhi);
+  if (qhi > lo || qhi <= qlo) return -1.f;
+  return gpow(lg, (float)(lo - qhi));
+}
+
+// `nz` = number of (sub-)segments in the launch (grid.z).  In state-only mode s_out receives
+// one local end state per z ([nz][B*H][dk][dv]); otherwise only the last segment writes s_out.
 cudaError_t launch_prefill_simt(const void* q, const void* k, const void* v, void* o,
                                 const float* log2g, const float* s_in, float* s_out,
                                 const ShapeArgs& s, int dtype, bool state_only,
-                                cudaStream_t stream);
+                                const SegArgs& sa, int nz, cudaStream_t stream);
 
 // Returns cudaErrorNotSupported when the shape is outside the TC kernel's envelope.
 cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void* o,
                               const float* log2g, const float* s_in, float* s_out,
-                              const ShapeArgs& s, bool state_only, cudaStream_t stream);
+                              const ShapeArgs& s, bool state_only, const SegArgs& sa, int nz,
+                              cudaStream_t stream);
+
+// State at token position `pos` from segment-local states (elementwise over [B*H][dk][dv]):
+//   out = gamma^pos * s_in + sum_{q : hi_q <= pos} gamma^(pos - hi_q) * loc[q]
+cudaError_t launch_state_at(const float* loc, const float* s_in, float* out, const SegArgs& sa,
+                            int64_t pos, const float* log2g, const ShapeArgs& s, cudaStream_t stream);
 bool tc_supported(const ShapeArgs& s, int dtype);
 void set_trace(void* buf);  // debug only: per-chunk clock64 trace of CTA (0,0), nullptr = off
 

@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(NT)
 prefill_simt_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
                     T* __restrict__ o, const float* __restrict__ log2g,
                     const float* __restrict__ s_in, float* __restrict__ s_out,
-                    int H, int N, int dk, int dv, int state_only) {
+                    int H, int N, int dk, int dv, int state_only, const SegArgs sa) {
   extern __shared__ float smem[];
   const int ldq = dk + 1;                     // padded rows: conflict-free column walks
   float* Qs = smem;                           // [CH][ldq]
@@ -35,19 +35,34 @@ prefill_simt_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* _
   const int nj = min(DVT, dv - j0);
   const int tid = threadIdx.x;
   const float lg = log2g[h];
+  int lo, hi;  // this CTA's token segment (SegArgs)
+  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
+  const size_t per_state = (size_t)gridDim.y * dk * dv;   // one [B*H][dk][dv] state
 
   const T* qb = q + (size_t)bh * N * dk;
   const T* kb = k + (size_t)bh * N * dk;
   const T* vb = v + (size_t)bh * N * dv;
   T* ob = o ? o + (size_t)bh * N * dv : nullptr;
 
-  for (int e = tid; e < dk * DVT; e += NT) {
-    const int i = e / DVT, j = e % DVT;
-    S[e] = (s_in && j < nj) ? s_in[((size_t)bh * dk + i) * dv + j0 + j] : 0.f;
+  {
+    const float w_in = gpow(lg, (float)lo);
+    for (int e = tid; e < dk * DVT; e += NT) {
+      const int i = e / DVT, j = e % DVT;
+      S[e] = (s_in && j < nj) ? w_in * s_in[((size_t)bh * dk + i) * dv + j0 + j] : 0.f;
+    }
+    for (int qi = 0; qi < sa.nloc; ++qi) {
+      const float wq = seg_loc_weight(sa, qi, N, lo, lg);
+      if (wq < 0.f) continue;
+      const float* lq = sa.loc + qi * per_state;
+      for (int e = tid; e < dk * DVT; e += NT) {
+        const int i = e / DVT, j = e % DVT;
+        if (j < nj) S[e] = fmaf(wq, lq[((size_t)bh * dk + i) * dv + j0 + j], S[e]);
+      }
+    }
   }
 
-  for (int c0 = 0; c0 < N; c0 += CH) {
-    const int L = min(CH, N - c0);
+  for (int c0 = lo; c0 < hi; c0 += CH) {
+    const int L = min(CH, hi - c0);
     __syncthreads();
     for (int e = tid; e < CH * dk; e += NT) {
       const int t = e / dk, i = e % dk;
@@ -99,10 +114,11 @@ prefill_simt_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* _
     }
   }
   __syncthreads();
-  if (s_out) {
+  if (s_out && (state_only || blockIdx.z == gridDim.z - 1)) {
+    float* so = s_out + (state_only ? blockIdx.z * per_state : 0);
     for (int e = tid; e < dk * DVT; e += NT) {
       const int i = e / DVT, j = e % DVT;
-      if (j < nj) s_out[((size_t)bh * dk + i) * dv + j0 + j] = S[e];
+      if (j < nj) so[((size_t)bh * dk + i) * dv + j0 + j] = S[e];
     }
   }
 }
@@ -112,12 +128,12 @@ prefill_simt_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* _
 cudaError_t launch_prefill_simt(const void* q, const void* k, const void* v, void* o,
                                 const float* log2g, const float* s_in, float* s_out,
                                 const ShapeArgs& s, int dtype, bool state_only,
-                                cudaStream_t stream) {
+                                const SegArgs& sa, int nz, cudaStream_t stream) {
   const size_t ldq = (size_t)s.dk + 1;
   const size_t smem = sizeof(float) * (2 * CH * ldq + CH * DVT + CH * (CH + 1) +
                                        (size_t)s.dk * DVT + CH);
   if (smem > 227 * 1024) return cudaErrorNotSupported;
-  dim3 grid((unsigned)((s.dv + DVT - 1) / DVT), (unsigned)(s.B * s.H));
+  dim3 grid((unsigned)((s.dv + DVT - 1) / DVT), (unsigned)(s.B * s.H), (unsigned)nz);
   cudaError_t err;
   if (dtype == LINATTN_BF16) {
     auto kern = prefill_simt_kernel<__nv_bfloat16>;
@@ -125,14 +141,14 @@ cudaError_t launch_prefill_simt(const void* q, const void* k, const void* v, voi
     if (err != cudaSuccess) return err;
     kern<<<grid, NT, smem, stream>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                      (const __nv_bfloat16*)v, (__nv_bfloat16*)o, log2g, s_in,
-                                     s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, state_only);
+                                     s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, state_only, sa);
   } else {
     auto kern = prefill_simt_kernel<float>;
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     kern<<<grid, NT, smem, stream>>>((const float*)q, (const float*)k, (const float*)v,
                                      (float*)o, log2g, s_in, s_out, (int)s.H, (int)s.N,
-                                     (int)s.dk, (int)s.dv, state_only);
+                                     (int)s.dk, (int)s.dv, state_only, sa);
   }
   count_launch();
   return cudaGetLastError();

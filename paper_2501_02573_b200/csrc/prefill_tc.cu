@@ -86,7 +86,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
                   const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
                   const float* __restrict__ log2g, const float* __restrict__ s_in,
                   float* __restrict__ s_out, int H, int N, int dv, int state_only,
-                  unsigned long long* __restrict__ trace) {
+                  const SegArgs sa, unsigned long long* __restrict__ trace) {
   using G = Cfg<DK, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -105,7 +105,10 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
   const uint32_t lane = threadIdx.x & 31;
   const int bh = blockIdx.y;
   const int j0 = blockIdx.x * kDVT;
-  const int nchunks = (N + kC - 1) / kC;
+  int lo, hi;  // this CTA's token segment (SegArgs)
+  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
+  const int nchunks = hi > lo ? (hi - lo + kC - 1) / kC : 0;
+  const size_t per_state = (size_t)gridDim.y * DK * dv;
   const float lg = log2g[bh % H];
 
   if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
@@ -146,13 +149,13 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         mbar_arrive_expect_tx(&full[s], bytes);
 #pragma unroll
         for (int kb = 0; kb < G::KB; ++kb) {
-          if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, c * kC, bh);
-          tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, c * kC, bh);
+          if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);
+          tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh);
         }
 #pragma unroll
         for (int nb = 0; nb < kDVT / 64; ++nb)
           tma_load_3d(st + G::Q_BYTES + G::K_BYTES + nb * 8192, &tm_v, &full[s], j0 + nb * 64,
-                      c * kC, bh);
+                      lo + c * kC, bh);
       }
     }
   } else if (warp == 9) {
@@ -216,7 +219,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     for (int c = 0; c < (state_only && warp < 2 ? 0 : nchunks); ++c) {
       const int s = c % STAGES;
       const int use = c / STAGES;
-      const int L = min(kC, N - c * kC);
+      const int L = min(kC, hi - lo - c * kC);
       mbar_wait(&full[s], use & 1);
       // MMA1 reads K unscaled: both the P^T warps and the K' warps wait for it
       if (!state_only) {
@@ -277,12 +280,25 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     const bool dv_ok = jd < dv;
     const uint32_t ta = tbase + ((sub * 32) << 16);
     {
-      const float carry = pw[min(kC, N)];
+      const float carry = pw[max(0, min(kC, hi - lo))];
+      const float w_in = gpow(lg, (float)lo);
       for (int cb = 0; cb < DK / 32; ++cb) {
         float sv[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          sv[i] = (s_in && dv_ok) ? s_in[((size_t)bh * DK + cb * 32 + i) * dv + jd] : 0.f;
+          sv[i] = (s_in && dv_ok) ? w_in * s_in[((size_t)bh * DK + cb * 32 + i) * dv + jd] : 0.f;
+        for (int qi = 0; qi < sa.nloc; ++qi) {
+          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
+          if (wq < 0.f || !dv_ok) continue;
+          const float* lq = sa.loc + qi * per_state + ((size_t)bh * DK + cb * 32) * dv + jd;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[i] = fmaf(wq, lq[(size_t)i * dv], sv[i]);
+        }
+        if (nchunks == 0 && s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1)) {
+          float* so = s_out + (state_only ? blockIdx.z * per_state : 0);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) so[((size_t)bh * DK + cb * 32 + i) * dv + jd] = sv[i];
+        }
         store_row_bf16_sw128(st_smem, kDVT * 128, d, cb * 32, sv);
 #pragma unroll
         for (int i = 0; i < 32; ++i) sv[i] *= carry;
@@ -294,13 +310,13 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       mbar_arrive(epi2_bar);
     }
     for (int c = 0; c < nchunks; ++c) {
-      const int L = min(kC, N - c * kC);
+      const int L = min(kC, hi - lo - c * kC);
       const bool last = c == nchunks - 1;
       mbar_wait(mma2_bar, c & 1);
       if (threadIdx.x == 128) LA_TRACE(7, c);
       tc_fence_after();
       if (!state_only) {
-        __nv_bfloat16* orow = o + ((size_t)bh * N + (size_t)c * kC) * dv + jd;
+        __nv_bfloat16* orow = o + ((size_t)bh * N + (size_t)lo + (size_t)c * kC) * dv + jd;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           float a[32], b[32];
@@ -320,9 +336,10 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         tmem_ld32(ta + T_S + cb * 32, sv);
         tmem_wait_ld();
         if (last) {
-          if (s_out && dv_ok) {
+          if (s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1)) {
+            float* so = s_out + (state_only ? blockIdx.z * per_state : 0);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) s_out[((size_t)bh * DK + cb * 32 + i) * dv + jd] = sv[i];
+            for (int i = 0; i < 32; ++i) so[((size_t)bh * DK + cb * 32 + i) * dv + jd] = sv[i];
           }
         } else {
           store_row_bf16_sw128(st_smem, kDVT * 128, d, cb * 32, sv);
@@ -403,15 +420,18 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                        const float* __restrict__ log2g, const float* __restrict__ s_in,
                        float* __restrict__ s_out, int H, int N, int dv, int state_only,
-                       unsigned long long* __restrict__ trace) {
+                       const SegArgs sa, unsigned long long* __restrict__ trace) {
   using G = Cfg<DK, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   uint64_t* empty = full + STAGES;
   uint64_t* mma1_bar = empty + STAGES;   // [2] P^T accumulator b ready
-  uint64_t* epi1_bar = mma1_bar + 2;     // [2] P^T smem b written, K' scaled     (64 or 128 arrivals)
-  uint64_t* mma_s_bar = epi1_bar + 2;    // dS_c ready
+  // [STAGES] stage s: P^T smem written, K' scaled (64 or 128 arrivals).  Indexed by stage, not
+  // by P^T buffer: in the state pass nothing else paces the K' warps, and a barrier indexed by
+  // c & 1 could complete two phases before the MMA warp observes the first (lapping).
+  uint64_t* epi1_bar = mma1_bar + 2;
+  uint64_t* mma_s_bar = epi1_bar + STAGES;  // dS_c ready
   uint64_t* ds_free = mma_s_bar + 1;     // dS read by the state warps            (256 arrivals)
   uint64_t* st_full = ds_free + 1;       // [2] S^T bf16 operand b published (TMEM) (256 arrivals)
   uint64_t* mma_o_bar = st_full + 2;     // [2] O accumulator b ready
@@ -426,7 +446,10 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   const uint32_t lane = threadIdx.x & 31;
   const int bh = blockIdx.y;
   const int j0 = blockIdx.x * kDVT;
-  const int nchunks = (N + kC - 1) / kC;
+  int lo, hi;  // this CTA's token segment (SegArgs); boundaries are multiples of kC except N
+  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
+  const int nchunks = hi > lo ? (hi - lo + kC - 1) / kC : 0;
+  const size_t per_state = (size_t)gridDim.y * DK * dv;
   const float lg = log2g[bh % H];
 
   if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
@@ -440,10 +463,10 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
+      mbar_init(&epi1_bar[i], state_only ? 64 : 128);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&mma1_bar[b], 1);
-      mbar_init(&epi1_bar[b], state_only ? 64 : 128);
       mbar_init(&o_free[b], 256);
       mbar_init(&mma_o_bar[b], 1);
     }
@@ -483,7 +506,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     for (int c = 0; c < (state_only && warp < 2 ? 0 : nchunks); ++c) {
       const int s = c % STAGES;
       const int b = c & 1;
-      const int L = min(kC, N - c * kC);
+      const int L = min(kC, hi - lo - c * kC);
       mbar_wait(&full[s], (c / STAGES) & 1);
       if (!state_only) {
         mbar_wait(&mma1_bar[b], (c >> 1) & 1);      // MMA1 has consumed the unscaled K
@@ -558,7 +581,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       fence_proxy_async_smem();
       tc_fence_before();
       if (tracing && lane == 0) trace[(warp < 2 ? 3 : 4) * 4096 + c] = clock64();
-      mbar_arrive(&epi1_bar[b]);
+      mbar_arrive(&epi1_bar[s]);
     }
   } else if (warp < 12) {
     // ------------------------------------------------------------ running state + outputs
@@ -576,8 +599,23 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     const uint32_t ta_o = tbase + ((uint32_t)d0 << 16);
     const bool leader = (warp == 4 && lane == 0);
     float S[SC];
+    {
+      // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs)
+      const float w_in = gpow(lg, (float)lo);
 #pragma unroll
-    for (int i = 0; i < SC; ++i) S[i] = (s_in && dv_ok) ? s_in[((size_t)bh * DK + col0 + i) * dv + jd] : 0.f;
+      for (int j = 0; j < SC; j += 16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          S[j + i] = (s_in && dv_ok) ? w_in * s_in[((size_t)bh * DK + col0 + j + i) * dv + jd] : 0.f;
+        for (int qi = 0; qi < sa.nloc; ++qi) {
+          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
+          if (wq < 0.f || !dv_ok) continue;
+          const float* lq = sa.loc + qi * per_state + ((size_t)bh * DK + col0 + j) * dv + jd;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) S[j + i] = fmaf(wq, lq[(size_t)i * dv], S[j + i]);
+        }
+      }
+    }
     // S (fp32 regs) -> bf16 pairs -> TMEM S^T operand buffer `buf` (row d, columns col0/2..)
     const uint32_t ta_st = tbase + ((sub * 32) << 16) + T_ST + col0 / 2;
     auto publish = [&](int buf) {
@@ -592,13 +630,25 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       tc_fence_before();
       mbar_arrive(&st_full[buf]);
     };
-    if (!state_only) publish(0);
+    // end state: state-only launches write one local state per segment, full launches only
+    // the last segment (whose seed already covers every earlier token)
+    float* const so = (s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1))
+                          ? s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)bh * DK + col0) * dv + jd
+                          : nullptr;
+#define LA_WRITE_STATE()                                          \
+  do {                                                            \
+    if (so != nullptr) {                                          \
+      _Pragma("unroll") for (int i = 0; i < SC; ++i) so[(size_t)i * dv] = S[i]; \
+    }                                                             \
+  } while (0)
+    if (nchunks == 0) LA_WRITE_STATE();
+    if (!state_only && nchunks > 0) publish(0);
     // stmatrix row address of this thread: matrix m = lane/8 of each x4 group, row lane%8
     const int mrow = lane & 7;
     const int mi = lane >> 3;                  // 0: (d0, t), 1: (d0+8, t), 2: (d0, t+8), 3: (d0+8, t+8)
     const int md = d0 + (mi & 1) * 8;          // 8-aligned dv row of the tile this address serves
     for (int c = 0; c < nchunks; ++c) {
-      const int L = min(kC, N - c * kC);
+      const int L = min(kC, hi - lo - c * kC);
       const int b = c & 1;
       mbar_wait(mma_s_bar, c & 1);
       tc_fence_after();
@@ -614,12 +664,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       tc_fence_before();
       mbar_arrive(ds_free);
       if (tracing && lane == 0 && sub == 0 && g == 0) trace[6 * 4096 + c] = clock64();
-      if (c == nchunks - 1) {
-        if (s_out && dv_ok) {
-#pragma unroll
-          for (int i = 0; i < SC; ++i) s_out[((size_t)bh * DK + col0 + i) * dv + jd] = S[i];
-        }
-      }
+      if (c == nchunks - 1) LA_WRITE_STATE();
       if (state_only) continue;
       if (c != nchunks - 1) {
         // buffer (c+1)&1 was last read by Ox_{c-1}, which precedes dS_c in the tensor pipe
@@ -659,8 +704,8 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       fence_proxy_async_smem();
       named_bar_sync(2, 256);
       if (leader) {
-        tma_store_3d(&tm_o, ot, j0, c * kC, bh);
-        tma_store_3d(&tm_o, ot + kC * 128, j0 + 64, c * kC, bh);
+        tma_store_3d(&tm_o, ot, j0, lo + c * kC, bh);
+        tma_store_3d(&tm_o, ot + kC * 128, j0 + 64, lo + c * kC, bh);
         bulk_commit();
       }
       if (tracing && lane == 0 && sub == 0 && g == 0) trace[5 * 4096 + c] = clock64();
@@ -679,30 +724,30 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
           if (kL2Ahead > 0 && c == 0) {  // warm L2 with the first chunks too
             for (int cp = 1; cp < STAGES + kL2Ahead && cp < nchunks; ++cp) {
               for (int kb = 0; kb < G::KB; ++kb) {
-                if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, cp * kC, bh);
-                tma_prefetch_l2_3d(&tm_k, kb * 64, cp * kC, bh);
+                if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, lo + cp * kC, bh);
+                tma_prefetch_l2_3d(&tm_k, kb * 64, lo + cp * kC, bh);
               }
-              for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, cp * kC, bh);
+              for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, lo + cp * kC, bh);
             }
           }
           mbar_arrive_expect_tx(&full[s], bytes);
           if (kL2Ahead > 0 && c + STAGES + kL2Ahead < nchunks) {  // keep HBM requests ahead of the smem ring
             const int cp = c + STAGES + kL2Ahead;
             for (int kb = 0; kb < G::KB; ++kb) {
-              if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, cp * kC, bh);
-              tma_prefetch_l2_3d(&tm_k, kb * 64, cp * kC, bh);
+              if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, lo + cp * kC, bh);
+              tma_prefetch_l2_3d(&tm_k, kb * 64, lo + cp * kC, bh);
             }
-            for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, cp * kC, bh);
+            for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, lo + cp * kC, bh);
           }
 #pragma unroll
           for (int kb = 0; kb < G::KB; ++kb) {
-            if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, c * kC, bh);
-            tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, c * kC, bh);
+            if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);
+            tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh);
           }
 #pragma unroll
           for (int nb = 0; nb < kDVT / 64; ++nb)
             tma_load_3d(st + G::Q_BYTES + G::K_BYTES + nb * 8192, &tm_v, &full[s], j0 + nb * 64,
-                        c * kC, bh);
+                        lo + c * kC, bh);
         }
       }
     } else if (warp == 13) {
@@ -729,7 +774,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         mma_commit_elect(&mma1_bar[c & 1]);
         if (tracing && lane == 0) trace[11 * 4096 + c] = clock64();
       };
-      if (!state_only) issue_mma1(0);
+      if (!state_only && nchunks > 0) issue_mma1(0);
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % STAGES;
         const int b = c & 1;
@@ -741,7 +786,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         } else {
           mbar_wait(&full[s], (c / STAGES) & 1);
         }
-        mbar_wait(&epi1_bar[b], (c >> 1) & 1);         // P^T_c in smem, K'_c scaled
+        mbar_wait(&epi1_bar[s], (c / STAGES) & 1);     // P^T_c in smem, K'_c scaled
         if (tracing && lane == 0) trace[12 * 4096 + c] = clock64();
         if (c > 0) mbar_wait(ds_free, (c - 1) & 1);    // state warps hold dS_{c-1}
         tc_fence_after();
@@ -817,7 +862,7 @@ bool make_map(CUtensorMap* map, const void* base, int64_t D, int64_t N, int64_t 
 template <int DK, int STAGES>
 cudaError_t launch_dk(const void* q, const void* k, const void* v, void* o, const float* log2g,
                       const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
-                      cudaStream_t stream) {
+                      const SegArgs& sa, int nz, cudaStream_t stream) {
   using G = Cfg<DK, STAGES>;
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
   CUtensorMap mq, mk, mv;
@@ -831,10 +876,10 @@ cudaError_t launch_dk(const void* q, const void* k, const void* v, void* o, cons
   auto kern = prefill_tc_kernel<DK, STAGES>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
-  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH);
+  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
   kern<<<grid, kThreads, G::SMEM, stream>>>(mq, mk, mv, (__nv_bfloat16*)o, log2g, s_in, s_out,
                                             (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
-                                            g_trace);
+                                            sa, g_trace);
   count_launch();
   return cudaGetLastError();
 }
@@ -842,7 +887,7 @@ cudaError_t launch_dk(const void* q, const void* k, const void* v, void* o, cons
 template <int DK, int STAGES>
 cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, const float* log2g,
                         const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
-                        cudaStream_t stream) {
+                        const SegArgs& sa, int nz, cudaStream_t stream) {
   using G = v2::Cfg<DK, STAGES>;
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
   CUtensorMap mq, mk, mv;
@@ -858,10 +903,10 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   auto kern = v2::prefill_tc_pipe_kernel<DK, STAGES>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
-  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH);
+  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
   kern<<<grid, v2::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out,
                                                 (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
-                                                g_trace);
+                                                sa, g_trace);
   count_launch();
   return cudaGetLastError();
 }
@@ -879,13 +924,14 @@ bool tc_supported(const ShapeArgs& s, int dtype) {
 
 cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void* o,
                               const float* log2g, const float* s_in, float* s_out,
-                              const ShapeArgs& s, bool state_only, cudaStream_t stream) {
+                              const ShapeArgs& s, bool state_only, const SegArgs& sa, int nz,
+                              cudaStream_t stream) {
   for (const void* p : {q, k, v, (const void*)o})
     if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return cudaErrorNotSupported;
   switch (s.dk) {
-    case 64: return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, state_only, stream);
-    case 128: return launch_pipe<128, 4>(q, k, v, o, log2g, s_in, s_out, s, state_only, stream);
-    case 256: return launch_dk<256, 1>(q, k, v, o, log2g, s_in, s_out, s, state_only, stream);
+    case 64: return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
+    case 128: return launch_pipe<128, 4>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
+    case 256: return launch_dk<256, 1>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
     default: return cudaErrorNotSupported;
   }
 }

@@ -44,7 +44,48 @@ __global__ void prefix_combine_kernel_scalar(const float* __restrict__ gathered,
   s_in[idx] = acc;
 }
 
+// out = gamma^pos s_in + sum_{q: hi_q <= pos} gamma^(pos - hi_q) loc[q], float4 over [B*H][dk][dv].
+__global__ void state_at_kernel(const float4* __restrict__ loc, const float4* __restrict__ s_in,
+                                float4* __restrict__ out, const SegArgs sa, int N, int pos,
+                                const float* __restrict__ log2g, int H, int64_t per_head4,
+                                int64_t per_state4) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= per_state4) return;
+  const float lg = log2g[(int)((idx / per_head4) % H)];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (s_in) {
+    const float w = gpow(lg, (float)pos);
+    const float4 x = s_in[idx];
+    acc = make_float4(w * x.x, w * x.y, w * x.z, w * x.w);
+  }
+  for (int q = 0; q < sa.nloc; ++q) {
+    const float w = seg_loc_weight(sa, q, N, pos, lg);
+    if (w < 0.f) continue;
+    const float4 x = loc[(int64_t)q * per_state4 + idx];
+    acc.x = fmaf(w, x.x, acc.x);
+    acc.y = fmaf(w, x.y, acc.y);
+    acc.z = fmaf(w, x.z, acc.z);
+    acc.w = fmaf(w, x.w, acc.w);
+  }
+  out[idx] = acc;
+}
+
 }  // namespace
+
+cudaError_t launch_state_at(const float* loc, const float* s_in, float* out, const SegArgs& sa,
+                            int64_t pos, const float* log2g, const ShapeArgs& s, cudaStream_t stream) {
+  const int64_t per_head = s.dk * s.dv;
+  if (per_head % 4 != 0) return cudaErrorNotSupported;
+  for (const void* p : {(const void*)loc, (const void*)s_in, (const void*)out})
+    if (reinterpret_cast<uintptr_t>(p) & 15) return cudaErrorNotSupported;
+  const int64_t n4 = s.B * s.H * per_head / 4;
+  constexpr int NT = 256;
+  state_at_kernel<<<(unsigned)((n4 + NT - 1) / NT), NT, 0, stream>>>(
+      (const float4*)loc, (const float4*)s_in, (float4*)out, sa, (int)s.N, (int)pos, log2g, (int)s.H,
+      per_head / 4, n4);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_prefix_combine(const float* gathered, float* s_in, const int64_t* seg_lens,
                                   int P, int rank, const float* log2g, const ShapeArgs& s,

@@ -105,20 +105,9 @@ def _to_device(x, dtype):
 
 
 def _seqpar(q, k, v, log2g, parts: int, kernel: str):
-    """Two-phase split on one device; the 'all-gather' is a stack of segment states."""
-    n = q.shape[2]
-    bounds = np.linspace(0, n, parts + 1).astype(int)
-    lens = [int(bounds[p + 1] - bounds[p]) for p in range(parts)]
-    segs = [(int(bounds[p]), int(bounds[p + 1])) for p in range(parts) if lens[p] > 0]
-    lens = [hi - lo for lo, hi in segs]
-    states = torch.stack([ops.state_pass(k[:, :, lo:hi].contiguous(), v[:, :, lo:hi].contiguous(),
-                                         log2g, kernel=kernel) for lo, hi in segs])
-    out = torch.empty_like(v)
-    for p, (lo, hi) in enumerate(segs):
-        s_in = ops.prefix_combine(states, lens, p, log2g) if p > 0 else None
-        out[:, :, lo:hi] = ops.prefill(q[:, :, lo:hi].contiguous(), k[:, :, lo:hi].contiguous(),
-                                       v[:, :, lo:hi].contiguous(), log2g, s_in=s_in, kernel=kernel)
-    return out
+    """Two-phase sequence split on one device: segment-local state pass, then every segment
+    seeded from the earlier ones and run in parallel (recursion cross term, kernels.py:185-189)."""
+    return ops.prefill(q, k, v, log2g, kernel=kernel, seq_split=max(1, parts))
 
 
 def _recurrent(q, k, v, log2g):

@@ -69,8 +69,24 @@ def log2_gamma(gammas, decay: bool = True, device=None) -> torch.Tensor:
     return t.to(device) if device is not None else t
 
 
-def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "auto"):
-    """O = (Q K^T (.) M_gamma) V on device; optional initial/end state (fp32)."""
+def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "auto",
+            seq_split: int | None = None):
+    """O = (Q K^T (.) M_gamma) V on device; optional initial/end state (fp32).
+
+    ``seq_split``: None lets the library split the sequence across SMs when batch x head
+    leaves them idle (``seq_plan``); 1 forces a single pass; P > 1 forces P segments
+    (two-phase: segment-local state pass, then every segment seeded in parallel).
+    """
+    if seq_split is not None and seq_split > 1:
+        n = q.shape[2]
+        seg = -(-n // seq_split)
+        seg = -(-seg // 64) * 64 if seg < n else n
+        nseg = -(-n // seg)
+        loc = state_pass_segmented(k, v, log2g, seg, m=1, nseg=nseg - 1, kernel=kernel) if nseg > 1 else None
+        return prefill_segmented(q, k, v, log2g, seg, loc=loc, loc_geom=(seg, 1), s_in=s_in, s_out=s_out,
+                                 out=out, kernel=kernel)
+    if seq_split == 1:
+        return prefill_segmented(q, k, v, log2g, q.shape[2], s_in=s_in, s_out=s_out, out=out, kernel=kernel)
     _require_cuda(q, k, v, log2g, s_in, s_out, out)
     if not (q.dtype == k.dtype == v.dtype):
         raise UsageError(f"dtype mismatch: q={q.dtype} k={k.dtype} v={v.dtype}")
@@ -102,6 +118,68 @@ def state_pass(k, v, log2g, *, s_out=None, kernel: str = "auto"):
     _lib.check(lib.linattn_state_pass(k.data_ptr(), v.data_ptr(), s_out.data_ptr(), log2g.data_ptr(),
                                       B, H, N, dk, dv, _dtype_code(k), _KERNELS[kernel], _stream()))
     return s_out
+
+
+def seq_plan(B: int, H: int, N: int, dk: int, dv: int, dtype=torch.bfloat16, kernel: str = "auto"):
+    """(seg_len, nseg, m, sub) the library uses to split a prefill of this shape on one device."""
+    plan = (ctypes.c_int64 * 4)()
+    lib = _lib.load()
+    _lib.check(lib.linattn_seq_plan(B, H, N, dk, dv, _DTYPES[dtype], _KERNELS[kernel], plan))
+    return tuple(int(x) for x in plan)
+
+
+def state_pass_segmented(k, v, log2g, seg_len: int, *, m: int = 1, nseg: int | None = None,
+                         kernel: str = "auto", out=None):
+    """Local end states of segments [p*seg_len, (p+1)*seg_len), each cut into m sub-segments.
+
+    Returns [nseg*m, B, H, dk, dv] fp32 (each sub-segment from a zero state).
+    """
+    _require_cuda(k, v, log2g, out)
+    B, H, N, dk = k.shape
+    dv = v.shape[3]
+    if nseg is None:
+        nseg = -(-N // seg_len)
+    if out is None:
+        out = torch.empty((nseg * m, B, H, dk, dv), dtype=torch.float32, device=k.device)
+    lib = _lib.load()
+    _lib.check(lib.linattn_state_pass_segmented(k.data_ptr(), v.data_ptr(), out.data_ptr(), log2g.data_ptr(),
+                                                B, H, N, dk, dv, _dtype_code(k), _KERNELS[kernel], seg_len,
+                                                m, nseg, _stream()))
+    return out
+
+
+def prefill_segmented(q, k, v, log2g, seg_len: int, *, loc=None, loc_geom=None, s_in=None, s_out=None,
+                      out=None, kernel: str = "auto"):
+    """Prefill with every seg_len-token segment in parallel, seeded from s_in and the local
+    states ``loc`` (from ``state_pass_segmented`` with geometry ``loc_geom = (seg_len, m)``)."""
+    _require_cuda(q, k, v, log2g, s_in, s_out, out, loc)
+    B, H, N, dk = q.shape
+    dv = v.shape[3]
+    if out is None:
+        out = torch.empty_like(v)
+    for st in (s_in, s_out):
+        if st is not None and (st.dtype != torch.float32 or tuple(st.shape) != (B, H, dk, dv)):
+            raise ShapeError(f"state must be float32 [B,H,dk,dv]={B, H, dk, dv}, got {tuple(st.shape)}")
+    lseg, lm = loc_geom if loc_geom is not None else (seg_len, 1)
+    nloc = 0 if loc is None else loc.shape[0]
+    lib = _lib.load()
+    _lib.check(lib.linattn_prefill_segmented(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                             log2g.data_ptr(), _ptr(s_in), _ptr(s_out), _ptr(loc), lseg, lm,
+                                             nloc, B, H, N, dk, dv, _dtype_code(q), _KERNELS[kernel],
+                                             seg_len, _stream()))
+    return out
+
+
+def state_at(loc, loc_geom, pos: int, log2g, n: int, *, s_in=None, out=None):
+    """gamma^pos s_in + sum over loc entries ending at or before pos of gamma^(pos - hi) loc[z]."""
+    _require_cuda(loc, log2g, s_in, out)
+    _, B, H, dk, dv = loc.shape
+    if out is None:
+        out = torch.empty((B, H, dk, dv), dtype=torch.float32, device=loc.device)
+    lib = _lib.load()
+    _lib.check(lib.linattn_state_at(loc.data_ptr(), loc_geom[0], loc_geom[1], loc.shape[0], _ptr(s_in),
+                                    out.data_ptr(), pos, log2g.data_ptr(), B, H, n, dk, dv, _stream()))
+    return out
 
 
 def prefix_combine(gathered, seg_lens, rank: int, log2g, *, s_in=None):

@@ -4,10 +4,12 @@ Algorithm (algebra = the reference recursion cross term,
 kernels.py:185-189, with gamma^t * gamma^(mid-s) = gamma^(t+1) * gamma^(mid-1-s)):
 
   1. rank p owns the contiguous token segment [lo_p, hi_p) of length L_p;
-     state pass (K4): S_p = sum_t gamma^(L_p-1-t) k_t^T v_t from zero state;
+     state pass (K4), split across the SMs: local states of sub-segments, combined into
+     S_p = sum_t gamma^(L_p-1-t) k_t^T v_t from zero state;
   2. one all-gather of the fp32 end states [B, H, dk, dv] (the only exchange);
   3. prefix combine (K5): S_in(p) = sum_{q<p} gamma^(sum_{q<m<p} L_m) S_q;
-  4. seeded chunked prefill of the segment from S_in(p).
+  4. seeded chunked prefill of the segment from S_in(p) and the sub-segment states, every
+     sub-segment in parallel.
 
 Every rank computes only its own segment; the gathered states are tiny
 (2 MiB per rank at H=32, d=128), so one collective suffices on NVSwitch.
@@ -34,19 +36,34 @@ def segment_bounds(n: int, parts: int):
 
 
 class CudaBackend:
-    """Product backend: the sm_100a kernels of liblinattn_b200.so."""
+    """Product backend: the sm_100a kernels of liblinattn_b200.so.
+
+    The local scan of a rank's segment is itself split across the SMs when batch x head
+    leaves them idle (the same two-phase algebra inside the device, ``ops.seq_plan``).
+    """
 
     def __init__(self, kernel: str = "auto"):
         self.kernel = kernel
 
-    def state_pass(self, k, v, log2g):
-        return ops.state_pass(k, v, log2g, kernel=self.kernel)
+    def local_states(self, k, v, log2g):
+        """Segment-local end states of this rank's tokens and their geometry (seg_len, m)."""
+        B, H, L, dk = k.shape
+        dv = v.shape[3]
+        seg, nseg, m, _ = ops.seq_plan(B, H, L, dk, dv, k.dtype, self.kernel)
+        if nseg == 1:
+            seg, m = L, 1
+        loc = ops.state_pass_segmented(k, v, log2g, seg, m=m, nseg=nseg, kernel=self.kernel)
+        return loc, (seg, m)
+
+    def state_at(self, loc, geom, pos, log2g):
+        return ops.state_at(loc, geom, pos, log2g, pos)
 
     def prefix_combine(self, gathered, seg_lens, rank, log2g):
         return ops.prefix_combine(gathered, seg_lens, rank, log2g)
 
-    def prefill(self, q, k, v, log2g, s_in):
-        return ops.prefill(q, k, v, log2g, s_in=s_in, kernel=self.kernel)
+    def prefill(self, q, k, v, log2g, s_in, loc, geom):
+        return ops.prefill_segmented(q, k, v, log2g, geom[0], loc=loc, loc_geom=geom, s_in=s_in,
+                                     kernel=self.kernel)
 
 
 def sp_prefill(q_seg, k_seg, v_seg, log2g, seg_lens, group=None, backend=None):
@@ -55,6 +72,9 @@ def sp_prefill(q_seg, k_seg, v_seg, log2g, seg_lens, group=None, backend=None):
     q_seg, k_seg: [B, H, L_p, dk]; v_seg: [B, H, L_p, dv] (this rank's tokens);
     seg_lens: list of every rank's segment length (same on all ranks).
     Returns this rank's output segment [B, H, L_p, dv].
+
+    Per rank: one state pass over K, V (0.5x of the prefill bytes), one all-gather of a
+    [B, H, dk, dv] fp32 state, one seeded prefill (1x) -- 1.5x the single-pass traffic.
     """
     backend = backend or CudaBackend()
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -63,7 +83,8 @@ def sp_prefill(q_seg, k_seg, v_seg, log2g, seg_lens, group=None, backend=None):
         raise ValueError(f"seg_lens has {len(seg_lens)} entries for world size {world}")
     if k_seg.shape[2] != seg_lens[rank]:
         raise ValueError(f"rank {rank} holds {k_seg.shape[2]} tokens, seg_lens says {seg_lens[rank]}")
-    local = backend.state_pass(k_seg, v_seg, log2g)              # [B, H, dk, dv] fp32
+    loc, geom = backend.local_states(k_seg, v_seg, log2g)         # segment-local, zero state
+    local = backend.state_at(loc, geom, k_seg.shape[2], log2g)     # this rank's end state [B,H,dk,dv]
     if world > 1:
         local = local.contiguous()
         flat = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
@@ -73,4 +94,4 @@ def sp_prefill(q_seg, k_seg, v_seg, log2g, seg_lens, group=None, backend=None):
     else:
         gathered = local[None]
     s_in = backend.prefix_combine(gathered, seg_lens, rank, log2g) if rank > 0 else None
-    return backend.prefill(q_seg, k_seg, v_seg, log2g, s_in)
+    return backend.prefill(q_seg, k_seg, v_seg, log2g, s_in, loc, geom)

@@ -1,0 +1,131 @@
+"""Sequence segments on one device: the split plan, the segmented C ABI and the SP pieces.
+
+The algebra is the reference recursion cross term (kernels.py:185-189) applied across
+segments; every result is checked against the f64 oracle (oracle/linattn_oracle.py) at
+the tolerances of test_gpu_parity.py (bf16 tensor cores 2e-2, fp32 FFMA 1e-4).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import linattn_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+TOL_F32 = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2501_02573_b200 import _lib, ops
+    _lib.load()
+    return ops
+
+
+def dev(x, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+
+
+def _inputs(B, H, N, dk, dv, seed, gam):
+    b, c, v = orc.gen_inputs(B, H, N, dk, dv, np.float32, seed)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    return b, c, v, orc.oracle_attn(b, c, v, gam, True)
+
+
+def test_seq_plan_shapes(ops):
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    seg, nseg, m, sub = ops.seq_plan(1, 32, 131072, 128, 128)        # configs[4] on one GPU
+    assert nseg > 1 and seg % 64 == 0 and nseg * 32 <= sms and sub % 64 == 0
+    assert ops.seq_plan(8, 32, 8192, 128, 128)[1] == 1                # configs[1]: units fill the SMs
+    assert ops.seq_plan(1, 1, 4096, 128, 128, torch.float32)[1] == 1  # fp32 parity mode never splits
+
+
+@pytest.mark.parametrize("dk,dv", [(128, 128), (64, 128), (256, 256)])
+def test_auto_split_matches_oracle(ops, dk, dv):
+    gam = [1 - 2.0 ** -5, 1 - 2.0 ** -12]
+    b, c, v, ref = _inputs(1, 2, 4096, dk, dv, 31, gam)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    q, k, vv = dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16)
+    s_out = torch.empty(1, 2, dk, dv, device="cuda")
+    out = ops.prefill(q, k, vv, l2, s_out=s_out)                     # library plan (split)
+    one = ops.prefill(q, k, vv, l2, seq_split=1)                      # single pass
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
+    assert orc.max_rel_error(one.float().cpu().numpy(), ref) <= TOL_BF16
+    ref_s = np.stack([[orc.segment_end_state(c[0, h], v[0, h], gam[h]) for h in range(2)]])
+    assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= 5e-3
+
+
+@pytest.mark.parametrize("seg_len,m", [(256, 1), (256, 2), (256, 3), (512, 4), (64, 1)])
+@pytest.mark.parametrize("mode", ["tc", "simt"])
+def test_segmented_geometries(ops, seg_len, m, mode):
+    """Ragged N, empty sub-segments (256/3 -> 128+128+0), s_in seeding and the end state."""
+    B, H, N, d = 2, 3, 1000, 128 if mode == "tc" else 64
+    gam = [0.0, 0.97, 1.0]
+    b, c, v = orc.gen_inputs(B, H, N, d, d, np.float32, 32)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    s0 = np.random.default_rng(5).standard_normal((B, H, d, d)).astype(np.float32) * 0.1
+    ref, ref_s = orc.seeded_blocked_attn(b, c, v, gam, True, s0.astype(np.float64), block=64)
+    dt, tol = (torch.bfloat16, TOL_BF16) if mode == "tc" else (torch.float32, TOL_F32)
+    kernel = "tc" if mode == "tc" else "simt"
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    q, k, vv = dev(b, dt), dev(c, dt), dev(v, dt)
+    nseg = -(-N // seg_len)
+    loc = ops.state_pass_segmented(k, vv, l2, seg_len, m=m, nseg=nseg, kernel=kernel)
+    s_out = torch.empty(B, H, d, d, device="cuda")
+    out = ops.prefill_segmented(q, k, vv, l2, seg_len, loc=loc, loc_geom=(seg_len, m), s_in=dev(s0),
+                                s_out=s_out, kernel=kernel)
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= tol
+    assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= (5e-3 if mode == "tc" else 1e-5)
+    # the state at N from the local states equals the seeded end state
+    end = ops.state_at(loc, (seg_len, m), N, l2, N, s_in=dev(s0))
+    assert orc.max_rel_error(end.cpu().numpy(), ref_s) <= (5e-3 if mode == "tc" else 1e-5)
+
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_sp_pieces_loopback(ops, parts):
+    """Multi-GPU SP with the all-gather replaced by a stack of per-rank end states."""
+    from paper_2501_02573_b200.sp import CudaBackend, segment_bounds
+    gam = [1 - 2.0 ** -4, 1 - 2.0 ** -14, 0.0]
+    b, c, v, ref = _inputs(1, 3, 3000, 128, 128, 33, gam)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    be = CudaBackend()
+    bounds = segment_bounds(3000, parts)
+    lens = [hi - lo for lo, hi in bounds]
+    segs = [[dev(x[:, :, lo:hi], torch.bfloat16) for x in (b, c, v)] for lo, hi in bounds]
+    locs = [be.local_states(k, vv, l2) for _, k, vv in segs]
+    ends = torch.stack([be.state_at(loc, geom, k.shape[2], l2) for (loc, geom), (_, k, _) in zip(locs, segs)])
+    outs = []
+    for r, ((q, k, vv), (loc, geom)) in enumerate(zip(segs, locs)):
+        s_in = be.prefix_combine(ends, lens, r, l2) if r > 0 else None
+        outs.append(be.prefill(q, k, vv, l2, s_in, loc, geom))
+    got = torch.cat(outs, dim=2).float().cpu().numpy()
+    assert orc.max_rel_error(got, ref) <= TOL_BF16
+
+
+def test_split_causality_and_linearity(ops):
+    """configs[4]-shaped heads at N=32768 (split by the plan): bitwise causality and linearity."""
+    torch.manual_seed(1)
+    B, H, N, d = 1, 8, 32768, 128
+    q = torch.randn(B, H, N, d, device="cuda", dtype=torch.bfloat16)
+    k, v = torch.randn_like(q), torch.randn_like(q)
+    gam = [1 - 2 ** (-5 - 10 * h / (H - 1)) for h in range(H)]
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    assert ops.seq_plan(B, H, N, d, d)[1] > 1
+    o = ops.prefill(q, k, v, l2)
+    assert torch.equal(ops.prefill(q, k, (2 * v).contiguous(), l2), 2 * o)
+    k2 = k.clone()
+    k2[:, :, 30000:] = torch.randn_like(k2[:, :, 30000:])
+    assert torch.equal(ops.prefill(q, k2, v, l2)[:, :, :30000], o[:, :, :30000])
+    one = ops.prefill(q, k, v, l2, seq_split=1)
+    assert orc.max_rel_error(o.float().cpu().numpy(), one.float().cpu().numpy()) <= TOL_BF16
+    # sampled head against the oracle over the last 4096 tokens, seeded with the exact prefix state
+    h = 3
+    qq, kk, vv = (x[0, h].float().cpu().numpy().astype(np.float64) for x in (q, k, v))
+    s_pre = orc.segment_end_state(kk[:N - 4096], vv[:N - 4096], gam[h])
+    ref, _ = orc.seeded_blocked_attn(qq[None, None, N - 4096:], kk[None, None, N - 4096:],
+                                     vv[None, None, N - 4096:], [gam[h]], True, s_pre[None, None], block=64)
+    assert orc.max_rel_error(o[0, h, N - 4096:].float().cpu().numpy(), ref[0, 0]) <= TOL_BF16
