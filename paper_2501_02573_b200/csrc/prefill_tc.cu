@@ -828,6 +828,375 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
 }  // namespace v2
 
+// ============================================================================================
+// dk = 256 (configs[2], RetNet-shaped heads).  The per-CTA state S^T [128 dv][256 dk] fp32 is
+// 128 KiB -- half the register file -- so it lives in TMEM and the tensor pipe accumulates
+// into it directly:
+//   state warps   S_c (TMEM fp32) -> bf16 S_c^T operand (TMEM) ; S <- gamma^L S (in place)
+//   MMA2          O^T  = V^T P^T + S_c^T Q'^T     (TS form: A = bf16 S^T from TMEM)
+//                 S^T += V^T K'                    (accumulates onto the rescaled state)
+// TMEM (512 cols): P^T 64 | O 64 | S fp32 256 | S^T bf16 128 -- single-buffered.  The chain
+// per chunk is {state warps: ld/st 128 KiB of TMEM} -> {MMA2}; MMA1 of the next chunk and the
+// mask / Q' / K' epilogue run in its shadow, outputs drain on their own warps.
+// Warp roles (448 threads): 0-1 P^T mask + Q', 2-3 K', 4-7 state, 8-11 outputs,
+// 12 TMA producer, 13 MMA issuer / TMEM owner.
+namespace v3 {
+
+constexpr int kThreads = 448;
+constexpr uint32_t T_P = 0, T_O = 64, T_S = 128, T_SB = 384;
+
+template <int DK, int STAGES>
+struct Cfg {
+  static constexpr int KB = DK / 64;
+  static constexpr int Q_BYTES = kC * DK * 2;
+  static constexpr int K_BYTES = kC * DK * 2;
+  static constexpr int V_BYTES = kC * kDVT * 2;
+  static constexpr int STAGE_BYTES = Q_BYTES + K_BYTES + V_BYTES;
+  static constexpr int PT_BYTES = kC * kC * 2;
+  static constexpr int OT_BYTES = kC * kDVT * 2;
+  static constexpr int OFF_PT = STAGES * STAGE_BYTES;
+  static constexpr int OFF_OT = OFF_PT + PT_BYTES;
+  static constexpr int OFF_POW = OFF_OT + OT_BYTES;
+  static constexpr int OFF_POW2 = OFF_POW + 128 * 4;
+  static constexpr int OFF_BAR = OFF_POW2 + 192 * 4;
+  static constexpr int SMEM = OFF_BAR + 512 + 1024;
+};
+
+// rows `srow` of a K-major SW128 bf16 tile with KB 64-column blocks: x *= (w, w) in place
+template <int KB>
+__device__ __forceinline__ void scale_rows_bf16(uint8_t* base, int srow, uint32_t w2) {
+#pragma unroll
+  for (int kb0 = 0; kb0 < KB; kb0 += 2) {
+    uint4 x[16];
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        x[kb * 8 + j] = *reinterpret_cast<const uint4*>(base + (kb0 + kb) * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4));
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint4 y = x[kb * 8 + j];
+        y.x = v2::hmul2_bf16(y.x, w2);
+        y.y = v2::hmul2_bf16(y.y, w2);
+        y.z = v2::hmul2_bf16(y.z, w2);
+        y.w = v2::hmul2_bf16(y.w, w2);
+        *reinterpret_cast<uint4*>(base + (kb0 + kb) * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4)) = y;
+      }
+  }
+}
+
+template <int DK, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                             const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                             const float* __restrict__ log2g, const float* __restrict__ s_in,
+                             float* __restrict__ s_out, int H, int N, int dv, int state_only,
+                             const SegArgs sa) {
+  using G = Cfg<DK, STAGES>;
+  static_assert(DK % 128 == 0, "Q'/K' scaling walks 64-column blocks in pairs");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* empty = full + STAGES;
+  uint64_t* epi1_bar = empty + STAGES;     // [STAGES] P^T smem written, Q'/K' scaled (64 or 128)
+  uint64_t* mma1_bar = epi1_bar + STAGES;  // P^T accumulator ready
+  uint64_t* st_full = mma1_bar + 1;        // S_c published as bf16 and rescaled    (128)
+  uint64_t* mma2_bar = st_full + 1;        // O_c and S_{c+1} ready
+  uint64_t* o_free = mma2_bar + 1;         // O drained by the output warps          (128)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
+  float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);
+  uint32_t* pw2 = reinterpret_cast<uint32_t*>(smem + G::OFF_POW2) + 64;
+  uint8_t* pt_smem = smem + G::OFF_PT;
+  uint8_t* ot_smem = smem + G::OFF_OT;
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int bh = blockIdx.y;
+  const int j0 = blockIdx.x * kDVT;
+  int lo, hi;
+  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
+  const int nchunks = hi > lo ? (hi - lo + kC - 1) / kC : 0;
+  const size_t per_state = (size_t)gridDim.y * DK * dv;
+  const float lg = log2g[bh % H];
+
+  if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
+  if (threadIdx.x < 192) {
+    const int k = (int)threadIdx.x - 64;
+    const float a = k >= 0 ? gpow(lg, (float)k) : 0.f;
+    const float b = k + 1 >= 0 ? gpow(lg, (float)(k + 1)) : 0.f;
+    pw2[k] = pack_bf16x2(a, b);
+  }
+  if (warp == 12 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&epi1_bar[i], state_only ? 64 : 128);
+    }
+    mbar_init(mma1_bar, 1);
+    mbar_init(st_full, 128);
+    mbar_init(mma2_bar, 1);
+    mbar_init(o_free, 128);
+    fence_barrier_init();
+    if (!state_only) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_o);
+    }
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+  }
+  if (warp == 13) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ P^T mask + Q' / K' scaling
+    for (int c = 0; c < (state_only && warp < 2 ? 0 : nchunks); ++c) {
+      const int s = c % STAGES;
+      const int L = min(kC, hi - lo - c * kC);
+      mbar_wait(&full[s], (c / STAGES) & 1);
+      if (!state_only) {
+        mbar_wait(mma1_bar, c & 1);                 // MMA1 has consumed the unscaled Q and K
+        tc_fence_after();
+      }
+      uint8_t* q_smem = smem + s * G::STAGE_BYTES;
+      if (warp < 2) {
+        const int srow = warp * 32 + lane;
+        const uint32_t ta = tbase + ((warp * 32) << 16) + T_P;
+        uint8_t* row = pt_smem + srow * 128;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float p[32];
+          tmem_ld32(ta + half * 32, p);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int t0 = half * 32 + 8 * j;
+            uint4 pk;
+            pk.x = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 0], p[8 * j + 1]), pw2[t0 + 0 - srow]);
+            pk.y = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 2], p[8 * j + 3]), pw2[t0 + 2 - srow]);
+            pk.z = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 4], p[8 * j + 5]), pw2[t0 + 4 - srow]);
+            pk.w = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 6], p[8 * j + 7]), pw2[t0 + 6 - srow]);
+            *reinterpret_cast<uint4*>(row + (((half * 4 + j) ^ (srow & 7)) << 4)) = pk;
+          }
+        }
+        const uint32_t w2 = pw2[srow + 1];           // Q'[t] = gamma^(t+1) Q[t]
+        scale_rows_bf16<G::KB>(q_smem, srow, (w2 & 0xFFFFu) | (w2 << 16));
+      } else {
+        const int srow = (warp - 2) * 32 + lane;     // K'[s] = gamma^(L-1-s) K[s], 0 past L
+        const uint32_t w2 = pw2[srow < L ? L - 1 - srow : -64];
+        scale_rows_bf16<G::KB>(q_smem + G::Q_BYTES, srow, (w2 & 0xFFFFu) | (w2 << 16));
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&epi1_bar[s]);
+    }
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ state (TMEM fp32)
+    const int sub = warp - 4;
+    const int jd = j0 + sub * 32 + lane;
+    const bool dv_ok = jd < dv;
+    const uint32_t ta_s = tbase + ((sub * 32) << 16) + T_S;
+    const uint32_t ta_sb = tbase + ((sub * 32) << 16) + T_SB;
+    float* const so = (s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1))
+                          ? s_out + (state_only ? blockIdx.z * per_state : 0) + (size_t)bh * DK * dv + jd
+                          : nullptr;
+    {
+      // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs)
+      const float w_in = gpow(lg, (float)lo);
+      for (int cb = 0; cb < DK / 32; ++cb) {
+        float sv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          sv[i] = (s_in && dv_ok) ? w_in * s_in[((size_t)bh * DK + cb * 32 + i) * dv + jd] : 0.f;
+        for (int qi = 0; qi < sa.nloc; ++qi) {
+          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
+          if (wq < 0.f || !dv_ok) continue;
+          const float* lq = sa.loc + qi * per_state + ((size_t)bh * DK + cb * 32) * dv + jd;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[i] = fmaf(wq, lq[(size_t)i * dv], sv[i]);
+        }
+        if (nchunks == 0) {
+          if (so) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = sv[i];
+          }
+        } else {
+          tmem_st32(ta_s + cb * 32, sv);
+        }
+      }
+      tmem_wait_st();
+    }
+    for (int c = 0; c < nchunks; ++c) {
+      const int L = min(kC, hi - lo - c * kC);
+      if (c > 0) {
+        mbar_wait(mma2_bar, (c - 1) & 1);            // S_c complete, bf16 operand free
+        tc_fence_after();
+      }
+      const float carry = pw[L];
+#pragma unroll 2
+      for (int cb = 0; cb < DK / 32; ++cb) {
+        float sv[32];
+        tmem_ld32(ta_s + cb * 32, sv);
+        tmem_wait_ld();
+        if (!state_only) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(sv[2 * i], sv[2 * i + 1]);
+          tmem_st16(ta_sb + cb * 16, pk);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[i] *= carry;
+        tmem_st32(ta_s + cb * 32, sv);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(st_full);
+    }
+    if (nchunks > 0 && so) {
+      mbar_wait(mma2_bar, (nchunks - 1) & 1);
+      tc_fence_after();
+      for (int cb = 0; cb < DK / 32; ++cb) {
+        float sv[32];
+        tmem_ld32(ta_s + cb * 32, sv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = sv[i];
+      }
+    }
+  } else if (warp < 12) {
+    // ------------------------------------------------------------ outputs
+    // O^T (TMEM, lane = dv row) -> bf16 -> smem [t][d] (stmatrix.trans, 128B swizzle) -> TMA store
+    const int sub = warp - 8;
+    const bool leader = (warp == 8 && lane == 0);
+    const int mrow = lane & 7;
+    const int mi = lane >> 3;
+    for (int c = 0; c < (state_only ? 0 : nchunks); ++c) {
+      mbar_wait(mma2_bar, c & 1);
+      tc_fence_after();
+      if (leader) bulk_wait_read<0>();               // the previous store has read the tile
+      named_bar_sync(1, 128);
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const int d0 = sub * 32 + g * 16;
+        const int md = d0 + (mi & 1) * 8;
+        const uint32_t ta_o = tbase + ((uint32_t)d0 << 16) + T_O;
+#pragma unroll
+        for (int q4 = 0; q4 < 2; ++q4) {
+          uint32_t ro[16];
+          tmem_ld_16x256b_x4(ta_o + q4 * 32, ro);
+          tmem_wait_ld();
+          uint32_t pk[8];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            pk[2 * r + 0] = pack_bf16x2(__uint_as_float(ro[4 * r + 0]), __uint_as_float(ro[4 * r + 1]));
+            pk[2 * r + 1] = pack_bf16x2(__uint_as_float(ro[4 * r + 2]), __uint_as_float(ro[4 * r + 3]));
+          }
+#pragma unroll
+          for (int rr = 0; rr < 4; rr += 2) {
+            const int tt = q4 * 32 + rr * 8 + (mi >> 1) * 8 + mrow;
+            const uint32_t addr = smem_u32(ot_smem + (md / 64) * (kC * 128) + tt * 128 +
+                                           ((((md % 64) >> 3) ^ (tt & 7)) << 4));
+            stmatrix_x4_trans(addr, pk[2 * rr + 0], pk[2 * rr + 1], pk[2 * rr + 2], pk[2 * rr + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(o_free);
+      fence_proxy_async_smem();
+      named_bar_sync(2, 128);
+      if (leader) {
+        tma_store_3d(&tm_o, ot_smem, j0, lo + c * kC, bh);
+        tma_store_3d(&tm_o, ot_smem + kC * 128, j0 + 64, lo + c * kC, bh);
+        bulk_commit();
+      }
+    }
+    if (leader) bulk_wait<0>();
+  } else if (warp == 12) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES + G::V_BYTES;
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % STAGES;
+        mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * G::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[s], bytes);
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb) {
+          if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);
+          tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh);
+        }
+#pragma unroll
+        for (int nb = 0; nb < kDVT / 64; ++nb)
+          tma_load_3d(st + G::Q_BYTES + G::K_BYTES + nb * 8192, &tm_v, &full[s], j0 + nb * 64, lo + c * kC, bh);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ MMA issuer (whole warp)
+    constexpr uint32_t id_qk = idesc_bf16(128, kC, false, false);   // P^T  = K Q^T
+    constexpr uint32_t id_vp = idesc_bf16(128, kC, true, true);     // O^T  = V^T P^T
+    constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // O^T += S^T(TMEM) Q'^T
+    constexpr uint32_t id_vk = idesc_bf16(128, DK, true, true);     // S^T += V^T K'
+    const uint32_t base_addr = smem_u32(smem);
+    const uint32_t pt_addr = smem_u32(pt_smem);
+    auto issue_mma1 = [&](int c) {
+      const int s = c % STAGES;
+      mbar_wait(&full[s], (c / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
+      const uint32_t k_addr = q_addr + G::Q_BYTES;
+#pragma unroll
+      for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16_ss_elect(tbase + T_P, smem_desc_sw128(k_addr + kb * 8192 + kk * 32, 16, 1024),
+                            smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_qk, (kb | kk) != 0);
+      mma_commit_elect(mma1_bar);
+    };
+    if (!state_only && nchunks > 0) issue_mma1(0);
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % STAGES;
+      const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
+      const uint32_t k_addr = q_addr + G::Q_BYTES;
+      const uint32_t v_addr = k_addr + G::K_BYTES;
+      if (state_only) mbar_wait(&full[s], (c / STAGES) & 1);
+      mbar_wait(&epi1_bar[s], (c / STAGES) & 1);      // P^T_c in smem, Q'_c and K'_c scaled
+      mbar_wait(st_full, c & 1);                      // S_c published (bf16) and rescaled
+      if (!state_only && c > 0) mbar_wait(o_free, (c - 1) & 1);
+      tc_fence_after();
+      if (!state_only) {
+#pragma unroll
+        for (int ks = 0; ks < kC / 16; ++ks)
+          mma_bf16_ss_elect(tbase + T_O, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
+                            smem_desc_sw128(pt_addr + ks * 2048, 8192, 1024), id_vp, ks != 0);
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16_ts_elect(tbase + T_O, tbase + T_SB + (kb * 4 + kk) * 8,
+                              smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq, 1);
+      }
+#pragma unroll
+      for (int ks = 0; ks < kC / 16; ++ks)
+        mma_bf16_ss_elect(tbase + T_S, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
+                          smem_desc_sw128(k_addr + ks * 2048, 8192, 1024), id_vk, 1);
+      mma_commit_elect(mma2_bar);
+      mma_commit_elect(&empty[s]);
+      if (!state_only && c + 1 < nchunks) issue_mma1(c + 1);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 13) tmem_dealloc<kTmemCols>(tbase);
+}
+
+}  // namespace v3
+
 // ---- host side ---------------------------------------------------------------------------
 
 unsigned long long* g_trace = nullptr;  // debug: set by linattn_debug_set_trace
@@ -911,6 +1280,32 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   return cudaGetLastError();
 }
 
+template <int DK, int STAGES>
+cudaError_t launch_tmem_state(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                              const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
+                              const SegArgs& sa, int nz, cudaStream_t stream) {
+  using G = v3::Cfg<DK, STAGES>;
+  static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
+  CUtensorMap mq, mk, mv;
+  const int64_t BH = s.B * s.H;
+  if (!make_map(&mk, k, s.dk, s.N, BH) || !make_map(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
+  if (state_only) {
+    mq = mk;
+  } else if (!make_map(&mq, q, s.dk, s.N, BH)) {
+    return cudaErrorInvalidValue;
+  }
+  CUtensorMap mo = mk;
+  if (!state_only && !make_map(&mo, o, s.dv, s.N, BH)) return cudaErrorInvalidValue;
+  auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  if (err != cudaSuccess) return err;
+  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
+  kern<<<grid, v3::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H, (int)s.N,
+                                                (int)s.dv, state_only ? 1 : 0, sa);
+  count_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 void set_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
@@ -931,7 +1326,7 @@ cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void*
   switch (s.dk) {
     case 64: return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
     case 128: return launch_pipe<128, 4>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
-    case 256: return launch_dk<256, 1>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
+    case 256: return launch_tmem_state<256, 2>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
     default: return cudaErrorNotSupported;
   }
 }
