@@ -188,6 +188,112 @@ def load_profile_traffic(kernel_key):
         return None
 
 
+def _time_events(fn, iters, barrier, max_over_ranks):
+    """Mean ms per call over `iters` calls, CUDA events on the current stream, max over ranks."""
+    import torch
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return max_over_ranks(e0.elapsed_time(e1) / iters)
+
+
+def bench_decode(args, ops, dev, g, hbm, barrier, max_over_ranks):
+    import torch
+    DB, DH, ddk, ddv = DEC["B"], DEC["H"], DEC["dk"], DEC["dv"]
+    T = max(64, args.decode_steps // 64 * 64)
+    state = torch.zeros(DB, DH, ddk, ddv, device=dev, dtype=torch.float32)
+    qd = torch.randn(DB, DH, ddk, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
+    kd = torch.randn(DB, DH, ddk, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
+    vd = torch.randn(DB, DH, ddv, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
+    od = torch.empty_like(vd)
+    l2d = ops.log2_gamma(gammas(DH), True, dev)
+    for _ in range(3):
+        ops.decode_step(qd, kd, vd, state, l2d, out=od)
+    torch.cuda.synchronize()
+    per_graph = 64
+    graph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            for _ in range(per_graph):
+                ops.decode_step(qd, kd, vd, state, l2d, out=od)
+    torch.cuda.current_stream().wait_stream(s)
+    graph.replay()
+    torch.cuda.synchronize()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    d0.record()
+    for _ in range(T // per_graph):
+        graph.replay()
+    d1.record()
+    torch.cuda.synchronize()
+    us = max_over_ranks(d0.elapsed_time(d1) * 1e3 / T)
+    dbytes = DB * DH * (2 * 4 * ddk * ddv + 2 * (2 * ddk + 2 * ddv))
+    gbs = dbytes / (us * 1e-6) / 1e9
+    return {"workload": f"configs[3] decode step B=256,H=32,d=128, fp32 state, bf16 q/k/v/o, {T} steps "
+                        "(CUDA graph of 64 steps)",
+            "us_per_step": us, "hbm_gbs": gbs, "frac_of_hbm": gbs / hbm,
+            "bytes_per_step": dbytes, "steps": T, "kernel": "decode_step"}
+
+
+def bench_cfg3(args, ops, dev, g, hbm, tc_burst, barrier, max_over_ranks):
+    """configs[2]: B=4, H=16, N=16384, dk=256, dv=512 bf16 (per GPU; weak scaling over ranks)."""
+    import torch
+    B, H, N, dk, dv = 4, 16, 16384, 256, 512
+    q = torch.randn(B, H, N, dk, device=dev, dtype=torch.bfloat16, generator=g)
+    k = torch.randn(B, H, N, dk, device=dev, dtype=torch.bfloat16, generator=g)
+    v = torch.randn(B, H, N, dv, device=dev, dtype=torch.bfloat16, generator=g)
+    out = torch.empty_like(v)
+    l2 = ops.log2_gamma(gammas(H), True, dev)
+    ms = _time_events(lambda: ops.prefill(q, k, v, l2, out=out), 20, barrier, max_over_ranks)
+    nbytes = B * H * N * ops.bytes_per_token_head(dk, dv)
+    flops = 2 * B * H * N * (C0 * (dk + dv) + 2 * dk * dv)
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    tf = flops / (ms * 1e-3) / 1e12
+    del q, k, v, out
+    return {"workload": "configs[2] B=4,H=16,N=16384,dk=256,dv=512 bf16 chunked prefill per GPU",
+            "ms_per_step": ms, "tokens_per_s": B * N / (ms * 1e-3), "hbm_gbs": gbs, "frac_of_hbm": gbs / hbm,
+            "tensor_tflops_c64": tf, "tensor_frac_of_burst": tf / tc_burst, "bytes_per_step": nbytes,
+            "kernel": "prefill_tc (dk=256: state in TMEM)"}
+
+
+def bench_seqpar(args, ops, dev, g, hbm, world, rank, barrier, max_over_ranks):
+    """configs[4]: B=1, H=32, N=131072, d=128 -- one job; N>1: sequence parallel over ranks."""
+    import torch
+    from paper_2501_02573_b200 import sp
+    B, H, N, d = 1, 32, 131072, 128
+    lo, hi = sp.segment_bounds(N, world)[rank]
+    lens = [b - a for a, b in sp.segment_bounds(N, world)]
+    q = torch.randn(B, H, hi - lo, d, device=dev, dtype=torch.bfloat16, generator=g)
+    k = torch.randn_like(q)
+    v = torch.randn_like(q)
+    l2 = ops.log2_gamma(gammas(H), True, dev)
+    if world == 1:
+        fn = lambda: ops.prefill(q, k, v, l2)   # noqa: E731  (sequence split inside the GPU)
+        how = "sequence split inside one GPU: segment state pass -> seeded segments in parallel"
+    else:
+        fn = lambda: sp.sp_prefill(q, k, v, l2, lens)   # noqa: E731
+        how = (f"sequence parallel over {world} GPUs: per-rank split state pass -> NCCL all_gather of "
+               "[B,H,dk,dv] fp32 end states -> prefix combine -> seeded split prefill")
+    ms = _time_events(fn, 20, barrier, max_over_ranks)
+    nbytes = B * H * N * ops.bytes_per_token_head(d, d)
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    plan = ops.seq_plan(B, H, hi - lo, d, d)
+    del q, k, v
+    return {"workload": f"configs[4] B=1,H=32,N=131072,d=128 bf16 prefill, {world} GPU(s), strong scaling",
+            "ms_per_step": ms, "tokens_per_s": N / (ms * 1e-3),
+            "hbm_gbs_single_pass_bytes": gbs, "frac_of_hbm_per_gpu": gbs / hbm / world,
+            "method": how, "per_rank_plan": {"seg_len": plan[0], "segments": plan[1], "state_pass_split": plan[2]}}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -257,7 +363,7 @@ def run_ours(args):
     tflops = flops_launch / (ms * 1e-3) / 1e12
 
     # e2e: public API with pinned host buffers, H2D + kernel + D2H in the timed region
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(3, min(args.steps, 10))
     qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
     oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
     inputs = la.AttnInputs(b=qh, c=kh, v=vh, gamma=gam, decay=True)
@@ -274,43 +380,12 @@ def run_ours(args):
     # decode step (configs[3]): 1024 single-token steps, state 256x32x128x128 fp32 (512 MiB)
     dec = None
     if not args.no_decode:
-        DB, DH, ddk, ddv = DEC["B"], DEC["H"], DEC["dk"], DEC["dv"]
-        T = max(64, args.decode_steps // 64 * 64)
-        state = torch.zeros(DB, DH, ddk, ddv, device=dev, dtype=torch.float32)
-        qd = torch.randn(DB, DH, ddk, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
-        kd = torch.randn(DB, DH, ddk, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
-        vd = torch.randn(DB, DH, ddv, device=dev, dtype=torch.bfloat16, generator=g) * 0.1
-        od = torch.empty_like(vd)
-        l2d = ops.log2_gamma(gammas(DH), True, dev)
-        for _ in range(3):
-            ops.decode_step(qd, kd, vd, state, l2d, out=od)
-        torch.cuda.synchronize()
-        per_graph = 64
-        graph = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            with torch.cuda.graph(graph, stream=s):
-                for _ in range(per_graph):
-                    ops.decode_step(qd, kd, vd, state, l2d, out=od)
-        torch.cuda.current_stream().wait_stream(s)
-        graph.replay()
-        torch.cuda.synchronize()
-        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        barrier()
-        d0.record()
-        for _ in range(T // per_graph):
-            graph.replay()
-        d1.record()
-        torch.cuda.synchronize()
-        us = max_over_ranks(d0.elapsed_time(d1) * 1e3 / T)
-        dbytes = DB * DH * (2 * 4 * ddk * ddv + 2 * (2 * ddk + 2 * ddv))
-        gbs = dbytes / (us * 1e-6) / 1e9
-        dec = {"workload": f"configs[3] decode step B=256,H=32,d=128, fp32 state, bf16 q/k/v/o, {T} steps "
-                           "(CUDA graph of 64 steps)",
-               "us_per_step": us, "hbm_gbs": gbs, "frac_of_hbm": gbs / hbm,
-               "bytes_per_step": dbytes, "steps": T}
-        del state, qd, kd, vd, od
+        dec = bench_decode(args, ops, dev, g, hbm, barrier, max_over_ranks)
+
+    # configs[2] (RetNet-shaped, dk=256, dv=512) prefill, and configs[4] long context: sequence
+    # split inside the GPU at N=1, sequence parallel over the ranks (one NCCL all-gather) at N>1
+    cfg3 = None if args.no_extra else bench_cfg3(args, ops, dev, g, hbm, tc_burst, barrier, max_over_ranks)
+    cfg5 = None if args.no_extra else bench_seqpar(args, ops, dev, g, hbm, world, rank, barrier, max_over_ranks)
 
     # CPU baseline (oracle port of the reference's CPU blocking route), rank 0 at N=1 only
     cpu = None
@@ -318,11 +393,18 @@ def run_ours(args):
         cores = cores_available()
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
         with mproc.get_context("spawn").Pool(cores) as pool:
-            cpu_sample(pool, cores)
-            cv, cdt, slices = cpu_sample(pool, cores, per_core=8, seed=77)
+            cpu_sample(pool, cores)                       # warm the workers
+            total_t, total_slices, rounds = 0.0, 0, 0
+            while total_t < args.cpu_seconds:             # ~10 s of CPU work by default
+                _, cdt, slices = cpu_sample(pool, cores, per_core=4, seed=77 + rounds)
+                total_t += cdt
+                total_slices += slices
+                rounds += 1
+        cv = total_slices / (B * H) * B * N / total_t
         cpu = {"value": cv, "unit": "tokens/s", "cores": cores, "kind": "port",
-               "sample": f"{slices} of {B * H} (b,h) slices of configs[1], f32 two-level-block chunk {C0} "
-                         f"(oracle/linattn_oracle.py), process pool x{cores}, {cdt:.1f} s"}
+               "sample": f"{total_slices} (b,h) slices of configs[1] ({total_slices / (B * H):.1f} x the batch), "
+                         f"f32 two-level-block chunk {C0} (oracle/linattn_oracle.py), process pool x{cores}, "
+                         f"{total_t:.1f} s"}
 
     kernel_name = ops.prefill_kernel_name(dk, dv, torch.bfloat16, kernel)
     line = {
@@ -339,10 +421,13 @@ def run_ours(args):
                      "tensor_tflops_c64": tflops, "tensor_frac_of_burst": tflops / tc_burst},
         "e2e": {"value": world * tokens_per_rank / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": 3 * B * H * N * dk * 2, "d2h_bytes_per_step": B * H * N * dv * 2,
-                "ms_per_step": e2e_s * 1e3, "api": "run_method(b200-chunked) on pinned host bf16 tensors"},
+                "ms_per_step": e2e_s * 1e3,
+                "api": "run_method(b200-chunked) on pinned host bf16 tensors (H2D | kernel | D2H overlapped per batch piece)"},
         "gpu_launches": int(max_over_ranks(launches)),
         "clocks": clk.summary(),
         "decode": dec,
+        "prefill_configs2": cfg3,
+        "seqpar_configs4": cfg5,
         "cpu_baseline": cpu,
     }
     if rank == 0:
@@ -360,6 +445,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU-baseline sample length")
+    ap.add_argument("--no-extra", action="store_true", help="skip the configs[2]/configs[4] sub-benchmarks")
     ap.add_argument("--decode-steps", type=int, default=DEC["steps"],
                     help="decode steps timed for the configs[3] sub-benchmark (multiple of 64)")
     args = ap.parse_args()

@@ -33,7 +33,7 @@ import numpy as np
 import torch
 
 from . import ops
-from .errors import UsageError
+from .errors import LinAttnError, UsageError
 from .tensor import AttnInputs, validate_inputs
 
 DEFAULT_MEM_CAP = 2 << 30  # kept for signature parity with the reference (oracle.py:16)
@@ -121,6 +121,63 @@ def _recurrent(q, k, v, log2g):
     return out
 
 
+def _pieces(batch: int, heads: int, target: int = 8):
+    """Independent (batch, head) pieces for host<->device overlap: whole batches if B > 1."""
+    if batch > 1:
+        n = min(batch, target)
+        edges = [round(i * batch / n) for i in range(n + 1)]
+        return [(slice(edges[i], edges[i + 1]), slice(None)) for i in range(n)]
+    n = min(heads, target)
+    edges = [round(i * heads / n) for i in range(n + 1)]
+    return [(slice(None), slice(edges[i], edges[i + 1])) for i in range(n)]
+
+
+def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
+    """Host tensors through the device in pieces: H2D(i+1) | prefill(i) | D2H(i-1) overlap.
+
+    Every (batch, head) slice is independent (kernels.py:273-280), so the batch is cut into
+    pieces on the batch axis (or the head axis when B == 1) and each piece runs on three
+    streams -- copy-in, compute (torch's current stream), copy-out -- ordered by events.
+    With pinned host buffers both PCIe directions and the kernel run concurrently.
+    """
+    b, c, v = (torch.from_numpy(np.ascontiguousarray(x)) if not isinstance(x, torch.Tensor) else x
+               for x in (inputs.b, inputs.c, inputs.v))
+    in_dtype = v.dtype
+    dev = torch.device("cuda", torch.cuda.current_device())
+    qd = torch.empty(b.shape, dtype=cdt, device=dev)
+    kd = torch.empty(c.shape, dtype=cdt, device=dev)
+    vd = torch.empty(v.shape, dtype=cdt, device=dev)
+    od = torch.empty(v.shape, dtype=cdt, device=dev)
+    if result is None:
+        result = torch.empty(v.shape, dtype=in_dtype)
+    log2g = ops.log2_gamma(inputs.gamma, inputs.decay, device=dev)
+    compute = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_in.wait_stream(compute)          # device buffers were allocated on the compute stream
+    done = []
+    for bs, hs in _pieces(v.shape[0], v.shape[1]):
+        loaded = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            for host, d in ((b, qd), (c, kd), (v, vd)):
+                src = host[bs, hs]
+                if src.dtype == cdt:
+                    d[bs, hs].copy_(src, non_blocking=True)
+                else:   # stage in the host dtype, cast on the device
+                    d[bs, hs].copy_(src.to(device=dev, non_blocking=True))
+            loaded.record(s_in)
+        compute.wait_event(loaded)
+        ops.prefill(qd[bs, hs], kd[bs, hs], vd[bs, hs], log2g[hs], out=od[bs, hs], kernel=kernel)
+        computed = torch.cuda.Event()
+        computed.record(compute)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(computed)
+            src = od[bs, hs] if in_dtype == cdt else od[bs, hs].to(in_dtype)
+            result[bs, hs].copy_(src, non_blocking=result.is_pinned())
+        done.append(computed)
+    s_out.synchronize()
+    return result
+
+
 def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None = None,
                validate: bool = True, out=None):
     """Run a concrete device method; returns (output, analytic opcount) (kernels.py:257-281).
@@ -141,6 +198,14 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
     host = not inputs.on_device
     torch_host = inputs.on_device and not inputs.v.is_cuda
     in_dtype = inputs.v.dtype
+    if torch_host and method in (MethodId.B200_CHUNKED, MethodId.B200_CHUNKED_F32):
+        if not torch.cuda.is_available():
+            raise LinAttnError("no CUDA device: the B200 path has no CPU fallback")
+        kernel = "auto" if method is MethodId.B200_CHUNKED else "simt"
+        res = _host_pipelined(inputs, cdt, kernel, out)
+        chunk = TC_CHUNK if method is MethodId.B200_CHUNKED else SIMT_CHUNK
+        return res, ops.chunked_opcount(inputs.batch, inputs.heads, inputs.seqlen, inputs.rank,
+                                        inputs.dim, inputs.decay, chunk)
     q = _to_device(inputs.b, cdt)
     k = _to_device(inputs.c, cdt)
     v = _to_device(inputs.v, cdt)

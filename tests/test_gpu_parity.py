@@ -255,3 +255,19 @@ def test_cfg3_shape_small_n(la):
     out = ops.prefill(dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16),
                       ops.log2_gamma(gam, True, "cuda"))
     assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("batch,heads,dt", [(3, 2, torch.bfloat16), (1, 5, torch.bfloat16), (2, 3, torch.float32)])
+def test_host_tensor_pipeline(la, batch, heads, dt):
+    """Host (pinned and pageable) torch tensors: piecewise H2D | kernel | D2H equals the device call."""
+    b, c, v = orc.gen_inputs(batch, heads, 300, 64, 128, np.float32, 15)
+    gam = [1 - 2.0 ** -(3 + h) for h in range(heads)]
+    method = la.MethodId.B200_CHUNKED if dt == torch.bfloat16 else la.MethodId.B200_CHUNKED_F32
+    hb, hc, hv = (torch.from_numpy(x).to(dt) for x in (b, c, v))
+    want, _ = la.run_method(method, la.make_inputs(hb.cuda(), hc.cuda(), hv.cuda(), gam, True))
+    pinned = [x.pin_memory() for x in (hb, hc, hv)]
+    out = torch.empty(hv.shape, dtype=dt).pin_memory()
+    got, ops = la.run_method(method, la.make_inputs(*pinned, gam, True), out=out)
+    assert got is out and ops > 0 and torch.equal(got, want.cpu())
+    got2, _ = la.run_method(method, la.make_inputs(hb, hc, hv, gam, True))
+    assert torch.equal(got2, want.cpu())
