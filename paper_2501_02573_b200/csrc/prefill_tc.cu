@@ -842,8 +842,18 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 // 12 TMA producer, 13 MMA issuer / TMEM owner.
 namespace v3 {
 
-constexpr int kThreads = 448;
+// Warp roles (512 threads = 4 warpgroups, 128 registers): 0-1 V' scaling and P^T mask,
+// 2 TMA producer, 3 MMA issuer / TMEM owner, 4-11 state (two per TMEM subpartition),
+// 12-15 inter-chunk column scaling and the output drain.  Pipe order per chunk:
+//   S update (V'^T K) -> O_inter = S^T Q^T (unscaled Q) -> MMA1(c+1) -> O_intra = V^T P^T.
+// Between O_inter and O_intra the aux warps scale O column t by gamma^(t+1) in TMEM (fp32),
+// so Q is never rescaled in shared memory (that rescale was 128 KiB of smem traffic a chunk).
+// The state warps publish bf16 S_{c+1} as soon as O_inter(c) has read the operand.
+constexpr int kThreads = 512;
 constexpr uint32_t T_P = 0, T_O = 64, T_S = 128, T_SB = 384;
+#ifndef V3_L2_AHEAD
+#define V3_L2_AHEAD 0
+#endif
 
 template <int DK, int STAGES>
 struct Cfg {
@@ -855,37 +865,37 @@ struct Cfg {
   static constexpr int PT_BYTES = kC * kC * 2;
   static constexpr int OT_BYTES = kC * kDVT * 2;
   static constexpr int OFF_PT = STAGES * STAGE_BYTES;
-  static constexpr int OFF_OT = OFF_PT + PT_BYTES;
+  static constexpr int OFF_VS = OFF_PT + 2 * PT_BYTES;         // V' = gamma^(L-1-s) V[s] (S update operand)
+  static constexpr int OFF_OT = OFF_VS + V_BYTES;
   static constexpr int OFF_POW = OFF_OT + OT_BYTES;
   static constexpr int OFF_POW2 = OFF_POW + 128 * 4;
   static constexpr int OFF_BAR = OFF_POW2 + 192 * 4;
   static constexpr int SMEM = OFF_BAR + 512 + 1024;
 };
 
-// rows `srow` of a K-major SW128 bf16 tile with KB 64-column blocks: x *= (w, w) in place
-template <int KB>
-__device__ __forceinline__ void scale_rows_bf16(uint8_t* base, int srow, uint32_t w2) {
+// dst row `row`, 64-column blocks [nb0, nb0 + NB) of a SW128 bf16 tile: dst = (w, w) * src
+template <int NB>
+__device__ __forceinline__ void scale_row_blocks(const uint8_t* src, uint8_t* dst, int row, int nb0, uint32_t w2) {
+  uint4 x[NB * 8];
 #pragma unroll
-  for (int kb0 = 0; kb0 < KB; kb0 += 2) {
-    uint4 x[16];
+  for (int kb = 0; kb < NB; ++kb)
 #pragma unroll
-    for (int kb = 0; kb < 2; ++kb)
+    for (int j = 0; j < 8; ++j)
+      x[kb * 8 + j] = *reinterpret_cast<const uint4*>(src + (nb0 + kb) * 8192 + row * 128 + ((j ^ (row & 7)) << 4));
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        x[kb * 8 + j] = *reinterpret_cast<const uint4*>(base + (kb0 + kb) * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4));
+  for (int kb = 0; kb < NB; ++kb)
 #pragma unroll
-    for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        uint4 y = x[kb * 8 + j];
-        y.x = v2::hmul2_bf16(y.x, w2);
-        y.y = v2::hmul2_bf16(y.y, w2);
-        y.z = v2::hmul2_bf16(y.z, w2);
-        y.w = v2::hmul2_bf16(y.w, w2);
-        *reinterpret_cast<uint4*>(base + (kb0 + kb) * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4)) = y;
-      }
-  }
+    for (int j = 0; j < 8; ++j) {
+      uint4 y = x[kb * 8 + j];
+      y.x = v2::hmul2_bf16(y.x, w2);
+      y.y = v2::hmul2_bf16(y.y, w2);
+      y.z = v2::hmul2_bf16(y.z, w2);
+      y.w = v2::hmul2_bf16(y.w, w2);
+      *reinterpret_cast<uint4*>(dst + (nb0 + kb) * 8192 + row * 128 + ((j ^ (row & 7)) << 4)) = y;
+    }
 }
+
+__device__ __forceinline__ uint32_t dup_lo(uint32_t w2) { return (w2 & 0xFFFFu) | (w2 << 16); }
 
 template <int DK, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -893,22 +903,28 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
                              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                              const float* __restrict__ log2g, const float* __restrict__ s_in,
                              float* __restrict__ s_out, int H, int N, int dv, int state_only,
-                             const SegArgs sa) {
+                             const SegArgs sa, unsigned long long* __restrict__ trace) {
   using G = Cfg<DK, STAGES>;
-  static_assert(DK % 128 == 0, "Q'/K' scaling walks 64-column blocks in pairs");
+  static_assert(DK % 128 == 0 && kDVT == 128, "layout: two state warps per TMEM subpartition");
+  constexpr int SCOL = DK / 2;                     // state columns per state warp
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   uint64_t* empty = full + STAGES;
-  uint64_t* epi1_bar = empty + STAGES;     // [STAGES] P^T smem written, Q'/K' scaled (64 or 128)
-  uint64_t* mma1_bar = epi1_bar + STAGES;  // P^T accumulator ready
-  uint64_t* st_full = mma1_bar + 1;        // S_c published as bf16 and rescaled    (128)
-  uint64_t* mma2_bar = st_full + 1;        // O_c and S_{c+1} ready
-  uint64_t* o_free = mma2_bar + 1;         // O drained by the output warps          (128)
+  uint64_t* pt_bar = empty + STAGES;       // [STAGES] P^T smem (buffer c&1) written (64)
+  uint64_t* vs_bar = pt_bar + STAGES;      // [STAGES] V' written                    (64)
+  uint64_t* mma1_bar = vs_bar + STAGES;    // P^T accumulator ready
+  uint64_t* st_done = mma1_bar + 1;        // S_c published (bf16) and rescaled     (256)
+  uint64_t* mma_s_bar = st_done + 1;       // S_{c+1} = gamma^L S_c + V'^T K done
+  uint64_t* ox_bar = mma_s_bar + 1;        // O_inter(c) done (bf16 S operand free)
+  uint64_t* ox_scaled = ox_bar + 1;        // O column t scaled by gamma^(t+1)       (128)
+  uint64_t* mma_o_bar = ox_scaled + 1;     // O_intra(c) done: O_c complete
+  uint64_t* o_free = mma_o_bar + 1;        // O drained                              (128)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
   float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);
   uint32_t* pw2 = reinterpret_cast<uint32_t*>(smem + G::OFF_POW2) + 64;
   uint8_t* pt_smem = smem + G::OFF_PT;
+  uint8_t* vs_smem = smem + G::OFF_VS;
   uint8_t* ot_smem = smem + G::OFF_OT;
 
   const uint32_t warp = warp_id();
@@ -928,15 +944,19 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     const float b = k + 1 >= 0 ? gpow(lg, (float)(k + 1)) : 0.f;
     pw2[k] = pack_bf16x2(a, b);
   }
-  if (warp == 12 && lane == 0) {
+  if (warp == 2 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
-      mbar_init(&epi1_bar[i], state_only ? 64 : 128);
+      mbar_init(&pt_bar[i], 64);
+      mbar_init(&vs_bar[i], 64);
     }
     mbar_init(mma1_bar, 1);
-    mbar_init(st_full, 128);
-    mbar_init(mma2_bar, 1);
+    mbar_init(st_done, 256);
+    mbar_init(mma_s_bar, 1);
+    mbar_init(ox_bar, 1);
+    mbar_init(ox_scaled, 128);
+    mbar_init(mma_o_bar, 1);
     mbar_init(o_free, 128);
     fence_barrier_init();
     if (!state_only) {
@@ -946,137 +966,77 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
   }
-  if (warp == 13) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 3) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  // debug: per-chunk clock64 of CTA (0,0,0), trace[event * 4096 + chunk]
+  const bool tracing = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+#define V3_TRACE(ev, c) do { if (tracing && lane == 0 && (c) < 4096) trace[(ev) * 4096 + (c)] = clock64(); } while (0)
 
-  if (warp < 4) {
-    // ------------------------------------------------------------ P^T mask + Q' / K' scaling
-    for (int c = 0; c < (state_only && warp < 2 ? 0 : nchunks); ++c) {
+  if (warp < 2) {
+    // ------------------------------------------------------------ P^T mask (TMEM lanes 0-63)
+    const int srow = warp * 32 + lane;
+    for (int c = 0; c < nchunks; ++c) {
       const int s = c % STAGES;
       const int L = min(kC, hi - lo - c * kC);
       mbar_wait(&full[s], (c / STAGES) & 1);
-      if (!state_only) {
-        mbar_wait(mma1_bar, c & 1);                 // MMA1 has consumed the unscaled Q and K
+      if (c > 0) {
+        mbar_wait(mma_s_bar, (c - 1) & 1);           // S update c-1 has consumed V'
         tc_fence_after();
       }
-      uint8_t* q_smem = smem + s * G::STAGE_BYTES;
-      if (warp < 2) {
-        const int srow = warp * 32 + lane;
-        const uint32_t ta = tbase + ((warp * 32) << 16) + T_P;
-        uint8_t* row = pt_smem + srow * 128;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float p[32];
-          tmem_ld32(ta + half * 32, p);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int t0 = half * 32 + 8 * j;
-            uint4 pk;
-            pk.x = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 0], p[8 * j + 1]), pw2[t0 + 0 - srow]);
-            pk.y = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 2], p[8 * j + 3]), pw2[t0 + 2 - srow]);
-            pk.z = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 4], p[8 * j + 5]), pw2[t0 + 4 - srow]);
-            pk.w = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 6], p[8 * j + 7]), pw2[t0 + 6 - srow]);
-            *reinterpret_cast<uint4*>(row + (((half * 4 + j) ^ (srow & 7)) << 4)) = pk;
-          }
-        }
-        const uint32_t w2 = pw2[srow + 1];           // Q'[t] = gamma^(t+1) Q[t]
-        scale_rows_bf16<G::KB>(q_smem, srow, (w2 & 0xFFFFu) | (w2 << 16));
-      } else {
-        const int srow = (warp - 2) * 32 + lane;     // K'[s] = gamma^(L-1-s) K[s], 0 past L
+      if (warp == 0) V3_TRACE(12, c);
+      {   // V'[s] = gamma^(L-1-s) V[s], 0 past L (row srow, both 64-column blocks)
         const uint32_t w2 = pw2[srow < L ? L - 1 - srow : -64];
-        scale_rows_bf16<G::KB>(q_smem + G::Q_BYTES, srow, (w2 & 0xFFFFu) | (w2 << 16));
+        scale_row_blocks<kDVT / 64>(smem + s * G::STAGE_BYTES + G::Q_BYTES + G::K_BYTES, vs_smem, srow, 0, dup_lo(w2));
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&vs_bar[s]);
+      if (warp == 0) V3_TRACE(7, c);
+      if (state_only) continue;
+      mbar_wait(mma1_bar, c & 1);
+      tc_fence_after();
+      if (warp == 0) V3_TRACE(11, c);
+      const uint32_t ta = tbase + ((warp * 32) << 16) + T_P;
+      uint8_t* row = pt_smem + (c & 1) * G::PT_BYTES + srow * 128;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float p[32];
+        tmem_ld32(ta + half * 32, p);
+        tmem_wait_ld();
+        if (warp == 0 && half == 0) V3_TRACE(2, c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t0 = half * 32 + 8 * j;
+          uint4 pk;
+          pk.x = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 0], p[8 * j + 1]), pw2[t0 + 0 - srow]);
+          pk.y = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 2], p[8 * j + 3]), pw2[t0 + 2 - srow]);
+          pk.z = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 4], p[8 * j + 5]), pw2[t0 + 4 - srow]);
+          pk.w = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 6], p[8 * j + 7]), pw2[t0 + 6 - srow]);
+          *reinterpret_cast<uint4*>(row + (((half * 4 + j) ^ (srow & 7)) << 4)) = pk;
+        }
       }
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(&epi1_bar[s]);
+      mbar_arrive(&pt_bar[s]);
+      if (warp == 0) V3_TRACE(14, c);
+      if (warp == 0) V3_TRACE(6, c);
     }
-  } else if (warp < 8) {
-    // ------------------------------------------------------------ state (TMEM fp32)
-    const int sub = warp - 4;
-    const int jd = j0 + sub * 32 + lane;
-    const bool dv_ok = jd < dv;
-    const uint32_t ta_s = tbase + ((sub * 32) << 16) + T_S;
-    const uint32_t ta_sb = tbase + ((sub * 32) << 16) + T_SB;
-    float* const so = (s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1))
-                          ? s_out + (state_only ? blockIdx.z * per_state : 0) + (size_t)bh * DK * dv + jd
-                          : nullptr;
-    {
-      // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs)
-      const float w_in = gpow(lg, (float)lo);
-      for (int cb = 0; cb < DK / 32; ++cb) {
-        float sv[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          sv[i] = (s_in && dv_ok) ? w_in * s_in[((size_t)bh * DK + cb * 32 + i) * dv + jd] : 0.f;
-        for (int qi = 0; qi < sa.nloc; ++qi) {
-          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
-          if (wq < 0.f || !dv_ok) continue;
-          const float* lq = sa.loc + qi * per_state + ((size_t)bh * DK + cb * 32) * dv + jd;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) sv[i] = fmaf(wq, lq[(size_t)i * dv], sv[i]);
-        }
-        if (nchunks == 0) {
-          if (so) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = sv[i];
-          }
-        } else {
-          tmem_st32(ta_s + cb * 32, sv);
-        }
-      }
-      tmem_wait_st();
-    }
-    for (int c = 0; c < nchunks; ++c) {
-      const int L = min(kC, hi - lo - c * kC);
-      if (c > 0) {
-        mbar_wait(mma2_bar, (c - 1) & 1);            // S_c complete, bf16 operand free
-        tc_fence_after();
-      }
-      const float carry = pw[L];
-#pragma unroll 2
-      for (int cb = 0; cb < DK / 32; ++cb) {
-        float sv[32];
-        tmem_ld32(ta_s + cb * 32, sv);
-        tmem_wait_ld();
-        if (!state_only) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(sv[2 * i], sv[2 * i + 1]);
-          tmem_st16(ta_sb + cb * 16, pk);
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) sv[i] *= carry;
-        tmem_st32(ta_s + cb * 32, sv);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(st_full);
-    }
-    if (nchunks > 0 && so) {
-      mbar_wait(mma2_bar, (nchunks - 1) & 1);
-      tc_fence_after();
-      for (int cb = 0; cb < DK / 32; ++cb) {
-        float sv[32];
-        tmem_ld32(ta_s + cb * 32, sv);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = sv[i];
-      }
-    }
-  } else if (warp < 12) {
-    // ------------------------------------------------------------ outputs
-    // O^T (TMEM, lane = dv row) -> bf16 -> smem [t][d] (stmatrix.trans, 128B swizzle) -> TMA store
-    const int sub = warp - 8;
-    const bool leader = (warp == 8 && lane == 0);
+  } else if (warp >= 12) {
+    // ------------------------------------------------------------ V', Q' scaling and outputs
+    const int sub = warp - 12;
+    const int tid = threadIdx.x - 12 * 32;           // 0..127
+    const int row = tid >> 1;                        // token row of the chunk
+    const int part = tid & 1;                        // which half of the 64-column blocks
+    const bool leader = (tid == 0);
     const int mrow = lane & 7;
     const int mi = lane >> 3;
-    for (int c = 0; c < (state_only ? 0 : nchunks); ++c) {
-      mbar_wait(mma2_bar, c & 1);
+    // O^T (TMEM, lane = dv row) -> bf16 -> smem [t][d] (stmatrix.trans, 128B swizzle) -> TMA store
+    auto drain_outputs = [&](int c) {
+      mbar_wait(mma_o_bar, c & 1);
       tc_fence_after();
+      if (sub == 0) V3_TRACE(13, c);
       if (leader) bulk_wait_read<0>();               // the previous store has read the tile
       named_bar_sync(1, 128);
 #pragma unroll
@@ -1106,6 +1066,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       }
       tc_fence_before();
       mbar_arrive(o_free);
+      if (sub == 0) V3_TRACE(8, c);
       fence_proxy_async_smem();
       named_bar_sync(2, 128);
       if (leader) {
@@ -1113,15 +1074,135 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         tma_store_3d(&tm_o, ot_smem + kC * 128, j0 + 64, lo + c * kC, bh);
         bulk_commit();
       }
+    };
+    for (int c = 0; c < (state_only ? 0 : nchunks); ++c) {
+      const int s = c % STAGES;
+      const int L = min(kC, hi - lo - c * kC);
+      uint8_t* stage = smem + s * G::STAGE_BYTES;
+      (void)L;
+      (void)stage;
+      (void)s;
+      {
+        // O_inter(c)[d][t] *= gamma^(t+1)  (fp32, in TMEM: lanes sub*32.., columns t)
+        mbar_wait(ox_bar, c & 1);
+        tc_fence_after();
+        const uint32_t ta_o = tbase + ((uint32_t)(sub * 32) << 16) + T_O;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float o[32];
+          tmem_ld32(ta_o + half * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] *= pw[half * 32 + i + 1];
+          tmem_st32(ta_o + half * 32, o);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(ox_scaled);
+        if (sub == 0) V3_TRACE(6, c);
+      }
+      drain_outputs(c);
     }
     if (leader) bulk_wait<0>();
-  } else if (warp == 12) {
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ state (TMEM fp32)
+    // warp (half, sub): TMEM lanes sub*32.. (dv rows), state columns [half*SCOL, +SCOL)
+    const int sub = (warp - 4) % 4;
+    const int col0 = ((warp - 4) / 4) * SCOL;
+    const int jd = j0 + sub * 32 + lane;
+    const bool dv_ok = jd < dv;
+    const uint32_t ta_s = tbase + ((sub * 32) << 16) + T_S + col0;
+    const uint32_t ta_sb = tbase + ((sub * 32) << 16) + T_SB + col0 / 2;
+    float* const so = (s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1))
+                          ? s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)bh * DK + col0) * dv + jd
+                          : nullptr;
+    {
+      // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs)
+      const float w_in = gpow(lg, (float)lo);
+      for (int cb = 0; cb < SCOL / 32; ++cb) {
+        float sv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          sv[i] = (s_in && dv_ok) ? w_in * s_in[((size_t)bh * DK + col0 + cb * 32 + i) * dv + jd] : 0.f;
+        for (int qi = 0; qi < sa.nloc; ++qi) {
+          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
+          if (wq < 0.f || !dv_ok) continue;
+          const float* lq = sa.loc + qi * per_state + ((size_t)bh * DK + col0 + cb * 32) * dv + jd;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[i] = fmaf(wq, lq[(size_t)i * dv], sv[i]);
+        }
+        if (nchunks == 0) {
+          if (so) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = sv[i];
+          }
+        } else {
+          tmem_st32(ta_s + cb * 32, sv);
+        }
+      }
+      tmem_wait_st();
+    }
+    for (int c = 0; c < nchunks; ++c) {
+      const int L = min(kC, hi - lo - c * kC);
+      if (c > 0) {
+        // S_c complete; in the full pass also O_inter(c-1) done (it follows the S update in
+        // the pipe), so the bf16 operand buffer is free and S_c can be published straight away
+        mbar_wait(state_only ? mma_s_bar : ox_bar, (c - 1) & 1);
+        tc_fence_after();
+      }
+      if (warp == 4) V3_TRACE(0, c);
+      const float carry = pw[L];
+#pragma unroll 1
+      for (int cb = 0; cb < SCOL / 32; ++cb) {
+        float sv[32];
+        tmem_ld32(ta_s + cb * 32, sv);
+        tmem_wait_ld();
+        if (!state_only) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(sv[2 * i], sv[2 * i + 1]);
+          tmem_st16(ta_sb + cb * 16, pk);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[i] *= carry;
+        tmem_st32(ta_s + cb * 32, sv);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(st_done);
+      if (warp == 4) V3_TRACE(1, c);
+    }
+    if (nchunks > 0 && so) {
+      mbar_wait(mma_s_bar, (nchunks - 1) & 1);
+      tc_fence_after();
+      for (int cb = 0; cb < SCOL / 32; ++cb) {
+        float sv[32];
+        tmem_ld32(ta_s + cb * 32, sv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = sv[i];
+      }
+    }
+  } else if (warp == 2) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES + G::V_BYTES;
+      auto prefetch_chunk = [&](int cp) {
+        for (int kb = 0; kb < G::KB; ++kb) {
+          if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, lo + cp * kC, bh);
+          tma_prefetch_l2_3d(&tm_k, kb * 64, lo + cp * kC, bh);
+        }
+        for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, lo + cp * kC, bh);
+      };
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % STAGES;
+        // two smem stages only (80 KiB each): keep HBM requests V3_L2_AHEAD chunks ahead in L2
+        if (c == 0) {
+          for (int cp = STAGES; cp < STAGES + V3_L2_AHEAD && cp < nchunks; ++cp) prefetch_chunk(cp);
+        }
+        if (c + STAGES + V3_L2_AHEAD - 1 < nchunks && c > 0) prefetch_chunk(c + STAGES + V3_L2_AHEAD - 1);
         mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
+        V3_TRACE(9, c);
         uint8_t* st = smem + s * G::STAGE_BYTES;
         mbar_arrive_expect_tx(&full[s], bytes);
 #pragma unroll
@@ -1135,13 +1216,15 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       }
     }
   } else {
-    // ------------------------------------------------------------ MMA issuer (whole warp)
+    // ------------------------------------------------------------ MMA issuer (warp 3)
+    // pipe order per chunk: S update (the serial chain) first, then O, then MMA1 of c+1
     constexpr uint32_t id_qk = idesc_bf16(128, kC, false, false);   // P^T  = K Q^T
     constexpr uint32_t id_vp = idesc_bf16(128, kC, true, true);     // O^T  = V^T P^T
-    constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // O^T += S^T(TMEM) Q'^T
-    constexpr uint32_t id_vk = idesc_bf16(128, DK, true, true);     // S^T += V^T K'
+    constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // O^T  = S^T(TMEM) Q^T
+    constexpr uint32_t id_vk = idesc_bf16(128, DK, true, true);     // S^T += V'^T K
     const uint32_t base_addr = smem_u32(smem);
     const uint32_t pt_addr = smem_u32(pt_smem);
+    const uint32_t vs_addr = smem_u32(vs_smem);
     auto issue_mma1 = [&](int c) {
       const int s = c % STAGES;
       mbar_wait(&full[s], (c / STAGES) & 1);
@@ -1155,6 +1238,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
           mma_bf16_ss_elect(tbase + T_P, smem_desc_sw128(k_addr + kb * 8192 + kk * 32, 16, 1024),
                             smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_qk, (kb | kk) != 0);
       mma_commit_elect(mma1_bar);
+      V3_TRACE(5, c);
     };
     if (!state_only && nchunks > 0) issue_mma1(0);
     for (int c = 0; c < nchunks; ++c) {
@@ -1162,37 +1246,48 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
       const uint32_t k_addr = q_addr + G::Q_BYTES;
       const uint32_t v_addr = k_addr + G::K_BYTES;
-      if (state_only) mbar_wait(&full[s], (c / STAGES) & 1);
-      mbar_wait(&epi1_bar[s], (c / STAGES) & 1);      // P^T_c in smem, Q'_c and K'_c scaled
-      mbar_wait(st_full, c & 1);                      // S_c published (bf16) and rescaled
-      if (!state_only && c > 0) mbar_wait(o_free, (c - 1) & 1);
+      V3_TRACE(10, c);
+      mbar_wait(&vs_bar[s], (c / STAGES) & 1);        // V'_c written (implies chunk c landed)
+      mbar_wait(st_done, c & 1);                      // S_c rescaled and published in TMEM
       tc_fence_after();
-      if (!state_only) {
 #pragma unroll
-        for (int ks = 0; ks < kC / 16; ++ks)
-          mma_bf16_ss_elect(tbase + T_O, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
-                            smem_desc_sw128(pt_addr + ks * 2048, 8192, 1024), id_vp, ks != 0);
+      for (int ks = 0; ks < kC / 16; ++ks)
+        mma_bf16_ss_elect(tbase + T_S, smem_desc_sw128(vs_addr + ks * 2048, 8192, 1024),
+                          smem_desc_sw128(k_addr + ks * 2048, 8192, 1024), id_vk, 1);
+      mma_commit_elect(mma_s_bar);
+      V3_TRACE(3, c);
+      if (!state_only) {
+        if (c > 0) {
+          mbar_wait(o_free, (c - 1) & 1);             // O_{c-1} drained
+          tc_fence_after();
+        }
 #pragma unroll
         for (int kb = 0; kb < G::KB; ++kb)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             mma_bf16_ts_elect(tbase + T_O, tbase + T_SB + (kb * 4 + kk) * 8,
-                              smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq, 1);
-      }
+                              smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq, (kb | kk) != 0);
+        mma_commit_elect(ox_bar);
+        mbar_wait(&pt_bar[s], (c / STAGES) & 1);      // P^T_c in smem: its TMEM copy is free
+        if (c + 1 < nchunks) issue_mma1(c + 1);
+        mbar_wait(ox_scaled, c & 1);                  // O_inter(c) scaled by gamma^(t+1)
+        tc_fence_after();
+        const uint32_t pt_addr_c = pt_addr + (c & 1) * G::PT_BYTES;
 #pragma unroll
-      for (int ks = 0; ks < kC / 16; ++ks)
-        mma_bf16_ss_elect(tbase + T_S, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
-                          smem_desc_sw128(k_addr + ks * 2048, 8192, 1024), id_vk, 1);
-      mma_commit_elect(mma2_bar);
+        for (int ks = 0; ks < kC / 16; ++ks)
+          mma_bf16_ss_elect(tbase + T_O, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
+                            smem_desc_sw128(pt_addr_c + ks * 2048, 8192, 1024), id_vp, 1);
+        mma_commit_elect(mma_o_bar);
+        V3_TRACE(4, c);
+      }
       mma_commit_elect(&empty[s]);
-      if (!state_only && c + 1 < nchunks) issue_mma1(c + 1);
     }
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 13) tmem_dealloc<kTmemCols>(tbase);
+  if (warp == 3) tmem_dealloc<kTmemCols>(tbase);
 }
 
 }  // namespace v3
@@ -1301,7 +1396,7 @@ cudaError_t launch_tmem_state(const void* q, const void* k, const void* v, void*
   if (err != cudaSuccess) return err;
   dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
   kern<<<grid, v3::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H, (int)s.N,
-                                                (int)s.dv, state_only ? 1 : 0, sa);
+                                                (int)s.dv, state_only ? 1 : 0, sa, g_trace);
   count_launch();
   return cudaGetLastError();
 }

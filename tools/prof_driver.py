@@ -1,12 +1,19 @@
-"""Minimal driver for ncu: configs[1] prefill launched 3 times (bf16, B=8,H=32,N=8192,d=128)."""
+"""Minimal driver for ncu: one prefill shape launched 3 times (bf16).
+
+PROF_SHAPE="B,H,N,dk[,dv]" (default configs[1] 8,32,8192,128); PROF_SPLIT=1 forces one pass.
+"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2501_02573_b200 import ops
-B, H, N, d = [int(x) for x in os.environ.get("PROF_SHAPE", "8,32,8192,128").split(",")]
-q = torch.randn(B, H, N, d, device="cuda", dtype=torch.bfloat16)
-k, v = torch.randn_like(q), torch.randn_like(q)
-l2 = ops.log2_gamma([1 - 2 ** (-5 - 10 * h / (H - 1)) for h in range(H)], True, "cuda")
+shape = [int(x) for x in os.environ.get("PROF_SHAPE", "8,32,8192,128").split(",")]
+B, H, N, dk = shape[:4]
+dv = shape[4] if len(shape) > 4 else dk
+q = torch.randn(B, H, N, dk, device="cuda", dtype=torch.bfloat16)
+k = torch.randn_like(q)
+v = torch.randn(B, H, N, dv, device="cuda", dtype=torch.bfloat16)
+l2 = ops.log2_gamma([1 - 2 ** (-5 - 10 * h / max(1, H - 1)) for h in range(H)], True, "cuda")
+split = 1 if os.environ.get("PROF_SPLIT") == "1" else None
 for _ in range(3):
-    ops.prefill(q, k, v, l2)
+    ops.prefill(q, k, v, l2, seq_split=split)
 torch.cuda.synchronize()
