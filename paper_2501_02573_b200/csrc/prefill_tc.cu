@@ -851,9 +851,10 @@ namespace v3 {
 // The state warps publish bf16 S_{c+1} as soon as O_inter(c) has read the operand.
 constexpr int kThreads = 512;
 constexpr uint32_t T_P = 0, T_O = 64, T_S = 128, T_SB = 384;
-#ifndef V3_L2_AHEAD
-#define V3_L2_AHEAD 0
-#endif
+
+// Two TMA rings: Q+K (STAGES x 64 KiB, released after O_inter) and V (VST x 16 KiB, released
+// after O_intra), so the next Q/K loads start a whole O_intra earlier than with one ring.
+constexpr int VST = 3;
 
 template <int DK, int STAGES>
 struct Cfg {
@@ -861,10 +862,11 @@ struct Cfg {
   static constexpr int Q_BYTES = kC * DK * 2;
   static constexpr int K_BYTES = kC * DK * 2;
   static constexpr int V_BYTES = kC * kDVT * 2;
-  static constexpr int STAGE_BYTES = Q_BYTES + K_BYTES + V_BYTES;
+  static constexpr int STAGE_BYTES = Q_BYTES + K_BYTES;
   static constexpr int PT_BYTES = kC * kC * 2;
   static constexpr int OT_BYTES = kC * kDVT * 2;
-  static constexpr int OFF_PT = STAGES * STAGE_BYTES;
+  static constexpr int OFF_V = STAGES * STAGE_BYTES;
+  static constexpr int OFF_PT = OFF_V + VST * V_BYTES;
   static constexpr int OFF_VS = OFF_PT + 2 * PT_BYTES;         // V' = gamma^(L-1-s) V[s] (S update operand)
   static constexpr int OFF_OT = OFF_VS + V_BYTES;
   static constexpr int OFF_POW = OFF_OT + OT_BYTES;
@@ -909,9 +911,11 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
   constexpr int SCOL = DK / 2;                     // state columns per state warp
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);   // Q/K ring
   uint64_t* empty = full + STAGES;
-  uint64_t* pt_bar = empty + STAGES;       // [STAGES] P^T smem (buffer c&1) written (64)
+  uint64_t* vfull = empty + STAGES;        // [VST] V ring
+  uint64_t* vempty = vfull + VST;
+  uint64_t* pt_bar = vempty + VST;         // [STAGES] P^T smem (buffer c&1) written (64)
   uint64_t* vs_bar = pt_bar + STAGES;      // [STAGES] V' written                    (64)
   uint64_t* mma1_bar = vs_bar + STAGES;    // P^T accumulator ready
   uint64_t* st_done = mma1_bar + 1;        // S_c published (bf16) and rescaled     (256)
@@ -951,6 +955,10 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       mbar_init(&pt_bar[i], 64);
       mbar_init(&vs_bar[i], 64);
     }
+    for (int i = 0; i < VST; ++i) {
+      mbar_init(&vfull[i], 1);
+      mbar_init(&vempty[i], 1);
+    }
     mbar_init(mma1_bar, 1);
     mbar_init(st_done, 256);
     mbar_init(mma_s_bar, 1);
@@ -981,7 +989,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % STAGES;
       const int L = min(kC, hi - lo - c * kC);
-      mbar_wait(&full[s], (c / STAGES) & 1);
+      mbar_wait(&vfull[c % VST], (c / VST) & 1);
       if (c > 0) {
         mbar_wait(mma_s_bar, (c - 1) & 1);           // S update c-1 has consumed V'
         tc_fence_after();
@@ -989,7 +997,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       if (warp == 0) V3_TRACE(12, c);
       {   // V'[s] = gamma^(L-1-s) V[s], 0 past L (row srow, both 64-column blocks)
         const uint32_t w2 = pw2[srow < L ? L - 1 - srow : -64];
-        scale_row_blocks<kDVT / 64>(smem + s * G::STAGE_BYTES + G::Q_BYTES + G::K_BYTES, vs_smem, srow, 0, dup_lo(w2));
+        scale_row_blocks<kDVT / 64>(smem + G::OFF_V + (c % VST) * G::V_BYTES, vs_smem, srow, 0, dup_lo(w2));
       }
       fence_proxy_async_smem();
       mbar_arrive(&vs_bar[s]);
@@ -1185,22 +1193,11 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     }
   } else if (warp == 2) {
     // ------------------------------------------------------------ TMA producer
+    // lane 0 streams the Q/K ring, lane 1 the V ring (independent waits)
     if (lane == 0) {
-      const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES + G::V_BYTES;
-      auto prefetch_chunk = [&](int cp) {
-        for (int kb = 0; kb < G::KB; ++kb) {
-          if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, lo + cp * kC, bh);
-          tma_prefetch_l2_3d(&tm_k, kb * 64, lo + cp * kC, bh);
-        }
-        for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, lo + cp * kC, bh);
-      };
+      const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES;
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % STAGES;
-        // two smem stages only (80 KiB each): keep HBM requests V3_L2_AHEAD chunks ahead in L2
-        if (c == 0) {
-          for (int cp = STAGES; cp < STAGES + V3_L2_AHEAD && cp < nchunks; ++cp) prefetch_chunk(cp);
-        }
-        if (c + STAGES + V3_L2_AHEAD - 1 < nchunks && c > 0) prefetch_chunk(c + STAGES + V3_L2_AHEAD - 1);
         mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
         V3_TRACE(9, c);
         uint8_t* st = smem + s * G::STAGE_BYTES;
@@ -1210,9 +1207,16 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
           if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);
           tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh);
         }
+      }
+    } else if (lane == 1) {
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % VST;
+        mbar_wait(&vempty[s], ((c / VST) & 1) ^ 1);
+        uint8_t* st = smem + G::OFF_V + s * G::V_BYTES;
+        mbar_arrive_expect_tx(&vfull[s], G::V_BYTES);
 #pragma unroll
         for (int nb = 0; nb < kDVT / 64; ++nb)
-          tma_load_3d(st + G::Q_BYTES + G::K_BYTES + nb * 8192, &tm_v, &full[s], j0 + nb * 64, lo + c * kC, bh);
+          tma_load_3d(st + nb * 8192, &tm_v, &vfull[s], j0 + nb * 64, lo + c * kC, bh);
       }
     }
   } else {
@@ -1245,9 +1249,10 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       const int s = c % STAGES;
       const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
       const uint32_t k_addr = q_addr + G::Q_BYTES;
-      const uint32_t v_addr = k_addr + G::K_BYTES;
+      const uint32_t v_addr = base_addr + G::OFF_V + (c % VST) * G::V_BYTES;
       V3_TRACE(10, c);
-      mbar_wait(&vs_bar[s], (c / STAGES) & 1);        // V'_c written (implies chunk c landed)
+      if (state_only) mbar_wait(&full[s], (c / STAGES) & 1);   // K_c landed (MMA1 waited otherwise)
+      mbar_wait(&vs_bar[s], (c / STAGES) & 1);        // V'_c written
       mbar_wait(st_done, c & 1);                      // S_c rescaled and published in TMEM
       tc_fence_after();
 #pragma unroll
@@ -1268,6 +1273,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
             mma_bf16_ts_elect(tbase + T_O, tbase + T_SB + (kb * 4 + kk) * 8,
                               smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq, (kb | kk) != 0);
         mma_commit_elect(ox_bar);
+        mma_commit_elect(&empty[s]);                  // Q_c, K_c consumed
         mbar_wait(&pt_bar[s], (c / STAGES) & 1);      // P^T_c in smem: its TMEM copy is free
         if (c + 1 < nchunks) issue_mma1(c + 1);
         mbar_wait(ox_scaled, c & 1);                  // O_inter(c) scaled by gamma^(t+1)
@@ -1279,8 +1285,10 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
                             smem_desc_sw128(pt_addr_c + ks * 2048, 8192, 1024), id_vp, 1);
         mma_commit_elect(mma_o_bar);
         V3_TRACE(4, c);
+      } else {
+        mma_commit_elect(&empty[s]);
       }
-      mma_commit_elect(&empty[s]);
+      mma_commit_elect(&vempty[c % VST]);             // V_c consumed (O_intra / V')
     }
   }
 
