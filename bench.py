@@ -304,10 +304,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LINATTN_BENCH_BACKEND=gloo runs the N>1 code path on a box with fewer GPUs than ranks
+    # (ranks share devices; a path check, not a measurement). The default is NCCL, one GPU each.
+    backend = os.environ.get("LINATTN_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     hbm, tc_burst, tc_sus, peak_kind = peaks()
 
     def barrier():
@@ -317,7 +325,7 @@ def run_ours(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

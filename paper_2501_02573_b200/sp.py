@@ -87,10 +87,13 @@ def sp_prefill(q_seg, k_seg, v_seg, log2g, seg_lens, group=None, backend=None):
     local = backend.state_at(loc, geom, k_seg.shape[2], log2g)     # this rank's end state [B,H,dk,dv]
     if world > 1:
         local = local.contiguous()
+        # gloo has no device all-gather: stage through the host (CPU tests, shared-GPU path checks)
+        host = local.is_cuda and dist.get_backend(group) == "gloo"
+        src = local.cpu() if host else local
         flat = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
-                           device=local.device)
-        dist.all_gather_into_tensor(flat, local, group=group)   # one collective; NCCL over NVLink
-        gathered = flat.view((world,) + tuple(local.shape))
+                           device=src.device)
+        dist.all_gather_into_tensor(flat, src, group=group)     # one collective; NCCL over NVLink
+        gathered = flat.view((world,) + tuple(local.shape)).to(local.device)
     else:
         gathered = local[None]
     s_in = backend.prefix_combine(gathered, seg_lens, rank, log2g) if rank > 0 else None
