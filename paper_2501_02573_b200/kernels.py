@@ -121,15 +121,15 @@ def _recurrent(q, k, v, log2g):
     return out
 
 
-def _pieces(batch: int, heads: int, target: int = 8):
-    """Independent (batch, head) pieces for host<->device overlap: whole batches if B > 1."""
-    if batch > 1:
-        n = min(batch, target)
-        edges = [round(i * batch / n) for i in range(n + 1)]
-        return [(slice(edges[i], edges[i + 1]), slice(None)) for i in range(n)]
-    n = min(heads, target)
-    edges = [round(i * heads / n) for i in range(n + 1)]
-    return [(slice(None), slice(edges[i], edges[i + 1])) for i in range(n)]
+def _pieces(batch: int, heads: int, target: int = 16):
+    """Independent (batch, head-range) pieces for host<->device overlap, about `target` of them.
+
+    Each piece is one batch index and a contiguous head range (contiguous in [B, H, N, d]),
+    so the first H2D and the last D2H -- the parts no overlap can hide -- shrink to 1/target.
+    """
+    per_b = max(1, min(heads, -(-target // batch)))          # head groups per batch index
+    edges = [round(i * heads / per_b) for i in range(per_b + 1)]
+    return [(slice(b, b + 1), slice(edges[i], edges[i + 1])) for b in range(batch) for i in range(per_b)]
 
 
 def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
