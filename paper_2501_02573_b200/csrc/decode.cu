@@ -9,8 +9,16 @@
 namespace linattn {
 namespace {
 
-constexpr int NT = 256;
-constexpr int RB = 8;  // state rows per thread per batch of in-flight loads
+// Block size / rows per batch of in-flight loads: swept on B200 (configs[3]): 128 x 8 keeps the
+// most 16-byte loads in flight per SM (small blocks -> more resident CTAs): 190 -> 168 us/step.
+#ifndef DEC_NT
+#define DEC_NT 128
+#endif
+#ifndef DEC_RB
+#define DEC_RB 8
+#endif
+constexpr int NT = DEC_NT;
+constexpr int RB = DEC_RB;  // state rows per thread per batch of in-flight loads
 
 template <typename T, int VEC>
 __global__ void __launch_bounds__(NT)

@@ -271,3 +271,37 @@ def test_host_tensor_pipeline(la, batch, heads, dt):
     assert got is out and ops > 0 and torch.equal(got, want.cpu())
     got2, _ = la.run_method(method, la.make_inputs(hb, hc, hv, gam, True))
     assert torch.equal(got2, want.cpu())
+
+
+def test_configs0_shape_fp32_and_bf16(la):
+    """BASELINE configs[0]: B=1, H=8, N=2048, d=64, fp32, per-head gamma (the reference's own
+    CPU blocking-vs-naive case): fp32 parity mode <= 1e-4 and the tensor-core path <= 2e-2
+    against the f64 oracle, and the reference blocking route (oracle port) agrees too."""
+    b, c, v = orc.gen_inputs(1, 8, 2048, 64, 64, np.float32, 2026)
+    gam = [1 - 2.0 ** (-5 - h) for h in range(8)]
+    ref = orc.oracle_attn(b, c, v, gam, True)
+    out, ops_count = la.run_method(la.MethodId.B200_CHUNKED_F32, la.make_inputs(b, c, v, gam, True))
+    assert out.dtype == np.float32 and orc.max_rel_error(out, ref) <= TOL_F32
+    assert orc.max_rel_error(orc.blocked_attn(b, c, v, gam, True, block=64), ref) <= 1e-5
+    auto = la.decode(la.make_inputs(b, c, v, gam, True))            # auto -> fp32 mode for f32 input
+    assert orc.max_rel_error(auto, ref) <= TOL_F32
+    bq, cq, vq = (orc.bf16_round(x) for x in (b, c, v))
+    ref16 = orc.oracle_attn(bq, cq, vq, gam, True)
+    out16, _ = la.run_method(la.MethodId.B200_CHUNKED,
+                             la.make_inputs(*(dev(x, torch.bfloat16) for x in (bq, cq, vq)), gam, True))
+    assert orc.max_rel_error(out16.float().cpu().numpy(), ref16) <= TOL_BF16
+
+
+@pytest.mark.parametrize("dk,dv", [(128, 192), (64, 64), (256, 128)])
+@pytest.mark.parametrize("decay", [True, False])
+def test_split_binary_mask_and_partial_dv_tile(la, dk, dv, decay):
+    """The library's own sequence split (B*H small) with a partial dv tile and the binary mask."""
+    from paper_2501_02573_b200 import ops
+    b, c, v = orc.gen_inputs(1, 2, 3000, dk, dv, np.float32, 41)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v) * 0.25
+    gam = [0.5, 1.0]
+    assert ops.seq_plan(1, 2, 3000, dk, dv)[1] > 1
+    ref = orc.oracle_attn(b, c, v, gam if decay else [1.0, 1.0], decay)
+    out = ops.prefill(dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16),
+                      ops.log2_gamma(gam, decay, "cuda"))
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
