@@ -142,8 +142,13 @@ class ClockSampler:
         self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         while not self._stop.is_set():
             mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            mem = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_MEM)
             mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            self.samples.append((time.perf_counter(), mhz, mask))
+            try:
+                watts = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+            except pynvml.NVMLError:
+                watts = None
+            self.samples.append((time.perf_counter(), mhz, mask, mem, watts))
             self._ready.set()
             self._stop.wait(0.002)
 
@@ -173,8 +178,12 @@ class ClockSampler:
         t0, t1 = getattr(self, "t_start", None), getattr(self, "t_end", None)
         inside = [s for s in self.samples if t0 is not None and t0 <= s[0] <= t1] or self.samples
         sm = [s[1] for s in inside]
+        mem = [s[3] for s in inside]
+        watts = [s[4] for s in inside if s[4] is not None]
         reasons = sorted({n for s in inside for n, bit in self.REASONS.items() if s[2] & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "mem_mhz": statistics.median(mem) if mem else None,
+                "power_w_max": max(watts) if watts else None,
                 "reasons": reasons, "samples": len(sm), "source": "nvml, 2 ms, inside the timed region"}
 
 

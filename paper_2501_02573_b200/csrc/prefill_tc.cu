@@ -388,8 +388,10 @@ constexpr int kThreads = 448;
 #define LA_L2_AHEAD 0
 #endif
 constexpr int kL2Ahead = LA_L2_AHEAD;   // chunks of L2 prefetch beyond the smem ring
-// TMEM column map: P^T x2 | O x2 | dS | S^T (bf16 A operand) x2
-constexpr uint32_t T_P = 0, T_O = 128, T_DS = 256, T_ST = 384;
+// TMEM column map: P^T | O_inter | O_intra x2 | dS | S^T (bf16 A operand) x2.  O_inter = S_c^T Q^T
+// is kept apart so gamma^(t+1) is applied in fp32 in the output epilogue instead of rescaling Q
+// in shared memory (a 32 KiB read-modify-write per chunk on the mask warps' path).
+constexpr uint32_t T_P = 0, T_OX = 64, T_O = 128, T_DS = 256, T_ST = 384;
 
 template <int DK, int STAGES>
 struct Cfg {
@@ -426,7 +428,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   uint64_t* empty = full + STAGES;
-  uint64_t* mma1_bar = empty + STAGES;   // [2] P^T accumulator b ready
+  uint64_t* mma1_bar = empty + STAGES;   // P^T accumulator ready (single buffer)
   // [STAGES] stage s: P^T smem written, K' scaled (64 or 128 arrivals).  Indexed by stage, not
   // by P^T buffer: in the state pass nothing else paces the K' warps, and a barrier indexed by
   // c & 1 could complete two phases before the MMA warp observes the first (lapping).
@@ -435,8 +437,9 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   uint64_t* ds_free = mma_s_bar + 1;     // dS read by the state warps            (256 arrivals)
   uint64_t* st_full = ds_free + 1;       // [2] S^T bf16 operand b published (TMEM) (256 arrivals)
   uint64_t* mma_o_bar = st_full + 2;     // [2] O accumulator b ready
-  uint64_t* o_free = mma_o_bar + 2;      // [2] O accumulators b drained          (256 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+  uint64_t* o_free = mma_o_bar + 2;      // [2] O_intra accumulator b drained     (256 arrivals)
+  uint64_t* ox_free = o_free + 2;        // O_inter accumulator drained            (256 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ox_free + 1);
   float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);
   uint32_t* pw2 = reinterpret_cast<uint32_t*>(smem + G::OFF_POW2) + 64;   // pw2[k], k in [-64, 127]
   uint8_t* pt_smem = smem + G::OFF_PT;
@@ -470,6 +473,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       mbar_init(&o_free[b], 256);
       mbar_init(&mma_o_bar[b], 1);
     }
+    mbar_init(ox_free, 256);
     mbar_init(mma_s_bar, 1);
     mbar_init(ds_free, 256);
     mbar_init(&st_full[0], 256);
@@ -509,13 +513,13 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       const int L = min(kC, hi - lo - c * kC);
       mbar_wait(&full[s], (c / STAGES) & 1);
       if (!state_only) {
-        mbar_wait(&mma1_bar[b], (c >> 1) & 1);      // MMA1 has consumed the unscaled K
+        mbar_wait(mma1_bar, c & 1);                 // MMA1 has consumed the unscaled K
         tc_fence_after();
       }
       if (warp < 2) {
         // P^T[s][t] *= gamma^(t-s) (t >= s), bf16: row s of the MN-major B operand of Oi
         const int srow = warp * 32 + lane;
-        const uint32_t ta = tbase + ((warp * 32) << 16) + T_P + b * kC;
+        const uint32_t ta = tbase + ((warp * 32) << 16) + T_P;
         uint8_t* row = pt_smem + b * G::PT_BYTES + srow * 128;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
@@ -533,27 +537,6 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
             *reinterpret_cast<uint4*>(row + (((half * 4 + j) ^ (srow & 7)) << 4)) = pk;
           }
         }
-        // Q'[t] = gamma^(t+1) Q[t] in place (rows >= L are TMA zero-fill and never stored)
-        const uint32_t w2 = pw2[srow + 1];
-        const uint32_t wq = (w2 & 0xFFFFu) | (w2 << 16);
-        uint8_t* q_smem = smem + s * G::STAGE_BYTES;
-        uint4 x[G::KB * 8];
-#pragma unroll
-        for (int kb = 0; kb < G::KB; ++kb)
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            x[kb * 8 + j] = *reinterpret_cast<const uint4*>(q_smem + kb * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4));
-#pragma unroll
-        for (int kb = 0; kb < G::KB; ++kb)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint4 y = x[kb * 8 + j];
-            y.x = hmul2_bf16(y.x, wq);
-            y.y = hmul2_bf16(y.y, wq);
-            y.z = hmul2_bf16(y.z, wq);
-            y.w = hmul2_bf16(y.w, wq);
-            *reinterpret_cast<uint4*>(q_smem + kb * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4)) = y;
-          }
       } else {
         // K'[s] = gamma^(L-1-s) K[s], zero beyond the ragged end (in place, bf16x2 multiplies)
         const int srow = (warp - 2) * 32 + lane;
@@ -680,18 +663,25 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       named_bar_sync(1, 256);
 #pragma unroll
       for (int q4 = 0; q4 < 2; ++q4) {           // tokens q4*32 .. q4*32+31
-        uint32_t ro[16];
+        uint32_t ro[16], rx[16];
         tmem_ld_16x256b_x4(ta_o + T_O + b * kC + q4 * 32, ro);
+        tmem_ld_16x256b_x4(ta_o + T_OX + q4 * 32, rx);
         tmem_wait_ld();
         if (q4 == 1) {
           tc_fence_before();
           mbar_arrive(&o_free[b]);
+          mbar_arrive(ox_free);
         }
         uint32_t pk[8];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {            // 8-token group r: t = q4*32 + 8r + tq + {0,1}
-          pk[2 * r + 0] = pack_bf16x2(__uint_as_float(ro[4 * r + 0]), __uint_as_float(ro[4 * r + 1]));
-          pk[2 * r + 1] = pack_bf16x2(__uint_as_float(ro[4 * r + 2]), __uint_as_float(ro[4 * r + 3]));
+          // O = Oi + gamma^(t+1) Ox, in fp32 (the inter-chunk weight, reference w_t kernels.py:125)
+          const int t0 = q4 * 32 + 8 * r + 2 * (lane & 3);
+          const float w0 = pw[t0 + 1], w1 = pw[t0 + 2];
+          pk[2 * r + 0] = pack_bf16x2(fmaf(w0, __uint_as_float(rx[4 * r + 0]), __uint_as_float(ro[4 * r + 0])),
+                                      fmaf(w1, __uint_as_float(rx[4 * r + 1]), __uint_as_float(ro[4 * r + 1])));
+          pk[2 * r + 1] = pack_bf16x2(fmaf(w0, __uint_as_float(rx[4 * r + 2]), __uint_as_float(ro[4 * r + 2])),
+                                      fmaf(w1, __uint_as_float(rx[4 * r + 3]), __uint_as_float(ro[4 * r + 3])));
         }
 #pragma unroll
         for (int rr = 0; rr < 4; rr += 2) {      // two 8-token groups per stmatrix.x4
@@ -754,7 +744,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       // ---------------------------------------------------------- MMA issuer (whole warp)
       constexpr uint32_t id_qk = idesc_bf16(128, kC, false, false);   // P^T = K Q^T
       constexpr uint32_t id_vp = idesc_bf16(128, kC, true, true);     // O^T  = V^T P^T
-      constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // O^T += S^T(TMEM) Q'^T
+      constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // Ox^T = S^T(TMEM) Q^T
       constexpr uint32_t id_vk = idesc_bf16(128, DK, true, true);     // dS^T = V^T K'
       const uint32_t base_addr = smem_u32(smem);
       const uint32_t pt_addr = smem_u32(pt_smem);
@@ -769,9 +759,9 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         for (int kb = 0; kb < G::KB; ++kb)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_bf16_ss_elect(tbase + T_P + (c & 1) * kC, smem_desc_sw128(k_addr + kb * 8192 + kk * 32, 16, 1024),
+            mma_bf16_ss_elect(tbase + T_P, smem_desc_sw128(k_addr + kb * 8192 + kk * 32, 16, 1024),
                               smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_qk, (kb | kk) != 0);
-        mma_commit_elect(&mma1_bar[c & 1]);
+        mma_commit_elect(mma1_bar);
         if (tracing && lane == 0) trace[11 * 4096 + c] = clock64();
       };
       if (!state_only && nchunks > 0) issue_mma1(0);
@@ -781,12 +771,8 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
         const uint32_t k_addr = q_addr + G::Q_BYTES;
         const uint32_t v_addr = k_addr + G::K_BYTES;
-        if (!state_only) {
-          if (c + 1 < nchunks) issue_mma1(c + 1);      // run ahead into the other P^T buffer
-        } else {
-          mbar_wait(&full[s], (c / STAGES) & 1);
-        }
-        mbar_wait(&epi1_bar[s], (c / STAGES) & 1);     // P^T_c in smem, K'_c scaled
+        if (state_only) mbar_wait(&full[s], (c / STAGES) & 1);
+        mbar_wait(&epi1_bar[s], (c / STAGES) & 1);     // P^T_c in smem (TMEM copy free), K'_c scaled
         if (tracing && lane == 0) trace[12 * 4096 + c] = clock64();
         if (c > 0) mbar_wait(ds_free, (c - 1) & 1);    // state warps hold dS_{c-1}
         tc_fence_after();
@@ -797,9 +783,11 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                             smem_desc_sw128(k_addr + ks * 2048, 8192, 1024), id_vk, ks != 0);
         mma_commit_elect(mma_s_bar);
         if (!state_only) {
+          if (c + 1 < nchunks) issue_mma1(c + 1);      // P^T TMEM consumed: run ahead
           mbar_wait(&st_full[b], (c >> 1) & 1);        // S_c (bf16) published in TMEM buffer b
           if (tracing && lane == 0) trace[14 * 4096 + c] = clock64();
           if (c >= 2) mbar_wait(&o_free[b], ((c >> 1) - 1) & 1);
+          if (c >= 1) mbar_wait(ox_free, (c - 1) & 1);
           tc_fence_after();
           if (tracing && lane == 0) trace[2 * 4096 + c] = clock64();
 #pragma unroll
@@ -810,8 +798,8 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
           for (int kb = 0; kb < G::KB; ++kb)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ts_elect(tbase + T_O + b * kC, tbase + T_ST + b * (DK / 2) + (kb * 4 + kk) * 8,
-                                smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq, 1);
+              mma_bf16_ts_elect(tbase + T_OX, tbase + T_ST + b * (DK / 2) + (kb * 4 + kk) * 8,
+                                smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq, (kb | kk) != 0);
           mma_commit_elect(&mma_o_bar[b]);
         }
         mma_commit_elect(&empty[s]);
