@@ -742,25 +742,29 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       }
     } else if (warp == 13) {
       // ---------------------------------------------------------- MMA issuer (whole warp)
+      // Descriptors are built once; a K step only adds (byte offset >> 4) to the start-address
+      // field (smem addresses < 256 KiB, so the 14-bit field never carries).
       constexpr uint32_t id_qk = idesc_bf16(128, kC, false, false);   // P^T = K Q^T
       constexpr uint32_t id_vp = idesc_bf16(128, kC, true, true);     // O^T  = V^T P^T
       constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // Ox^T = S^T(TMEM) Q^T
       constexpr uint32_t id_vk = idesc_bf16(128, DK, true, true);     // dS^T = V^T K'
       const uint32_t base_addr = smem_u32(smem);
-      const uint32_t pt_addr = smem_u32(pt_smem);
+      const uint64_t dq0 = smem_desc_sw128(base_addr, 16, 1024);                          // K-major rows
+      const uint64_t dmn0 = smem_desc_sw128(base_addr, 8192, 1024);                       // MN-major
+      const uint64_t dpt0 = smem_desc_sw128(smem_u32(pt_smem), 8192, 1024);
+      constexpr uint64_t kStage = G::STAGE_BYTES >> 4, kQ = G::Q_BYTES >> 4, kK = G::K_BYTES >> 4;
       auto issue_mma1 = [&](int c) {
         const int s = c % STAGES;
         mbar_wait(&full[s], (c / STAGES) & 1);
         if (tracing && lane == 0) trace[10 * 4096 + c] = clock64();
         tc_fence_after();
-        const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
-        const uint32_t k_addr = q_addr + G::Q_BYTES;
+        const uint64_t dq = dq0 + s * kStage, dk = dq + kQ;
 #pragma unroll
         for (int kb = 0; kb < G::KB; ++kb)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_bf16_ss_elect(tbase + T_P, smem_desc_sw128(k_addr + kb * 8192 + kk * 32, 16, 1024),
-                              smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_qk, (kb | kk) != 0);
+            mma_bf16_ss_elect(tbase + T_P, dk + (kb * 512 + kk * 2), dq + (kb * 512 + kk * 2), id_qk,
+                              (kb | kk) != 0);
         mma_commit_elect(mma1_bar);
         if (tracing && lane == 0) trace[11 * 4096 + c] = clock64();
       };
@@ -768,38 +772,39 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % STAGES;
         const int b = c & 1;
-        const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
-        const uint32_t k_addr = q_addr + G::Q_BYTES;
-        const uint32_t v_addr = k_addr + G::K_BYTES;
+        const uint64_t dq = dq0 + s * kStage;                 // Q, K-major
+        const uint64_t dv_mn = dmn0 + s * kStage + kQ + kK;   // V, MN-major (A of V^T x)
+        const uint64_t dk_mn = dmn0 + s * kStage + kQ;        // K', MN-major (B of V^T K')
         if (state_only) mbar_wait(&full[s], (c / STAGES) & 1);
         mbar_wait(&epi1_bar[s], (c / STAGES) & 1);     // P^T_c in smem (TMEM copy free), K'_c scaled
         if (tracing && lane == 0) trace[12 * 4096 + c] = clock64();
+        // P^T TMEM is free again: start MMA1 of the next chunk before this chunk's dS, so its
+        // mask epilogue overlaps the state chain instead of following it
+        if (!state_only && c + 1 < nchunks) issue_mma1(c + 1);
         if (c > 0) mbar_wait(ds_free, (c - 1) & 1);    // state warps hold dS_{c-1}
         tc_fence_after();
         if (tracing && lane == 0) trace[1 * 4096 + c] = clock64();
 #pragma unroll
         for (int ks = 0; ks < kC / 16; ++ks)
-          mma_bf16_ss_elect(tbase + T_DS, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
-                            smem_desc_sw128(k_addr + ks * 2048, 8192, 1024), id_vk, ks != 0);
+          mma_bf16_ss_elect(tbase + T_DS, dv_mn + ks * 128, dk_mn + ks * 128, id_vk, ks != 0);
         mma_commit_elect(mma_s_bar);
         if (!state_only) {
-          if (c + 1 < nchunks) issue_mma1(c + 1);      // P^T TMEM consumed: run ahead
           mbar_wait(&st_full[b], (c >> 1) & 1);        // S_c (bf16) published in TMEM buffer b
           if (tracing && lane == 0) trace[14 * 4096 + c] = clock64();
           if (c >= 2) mbar_wait(&o_free[b], ((c >> 1) - 1) & 1);
           if (c >= 1) mbar_wait(ox_free, (c - 1) & 1);
           tc_fence_after();
           if (tracing && lane == 0) trace[2 * 4096 + c] = clock64();
+          const uint64_t dpt = dpt0 + b * (G::PT_BYTES >> 4);
 #pragma unroll
           for (int ks = 0; ks < kC / 16; ++ks)
-            mma_bf16_ss_elect(tbase + T_O + b * kC, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
-                              smem_desc_sw128(pt_addr + b * G::PT_BYTES + ks * 2048, 8192, 1024), id_vp, ks != 0);
+            mma_bf16_ss_elect(tbase + T_O + b * kC, dv_mn + ks * 128, dpt + ks * 128, id_vp, ks != 0);
 #pragma unroll
           for (int kb = 0; kb < G::KB; ++kb)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               mma_bf16_ts_elect(tbase + T_OX, tbase + T_ST + b * (DK / 2) + (kb * 4 + kk) * 8,
-                                smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq, (kb | kk) != 0);
+                                dq + (kb * 512 + kk * 2), id_sq, (kb | kk) != 0);
           mma_commit_elect(&mma_o_bar[b]);
         }
         mma_commit_elect(&empty[s]);
