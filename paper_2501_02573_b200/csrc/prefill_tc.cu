@@ -1219,30 +1219,33 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     constexpr uint32_t id_vp = idesc_bf16(128, kC, true, true);     // O^T  = V^T P^T
     constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // O^T  = S^T(TMEM) Q^T
     constexpr uint32_t id_vk = idesc_bf16(128, DK, true, true);     // S^T += V'^T K
+    // descriptors built once; K steps add (byte offset >> 4) to the start-address field
     const uint32_t base_addr = smem_u32(smem);
-    const uint32_t pt_addr = smem_u32(pt_smem);
-    const uint32_t vs_addr = smem_u32(vs_smem);
+    const uint64_t dq0 = smem_desc_sw128(base_addr, 16, 1024);
+    const uint64_t dmn0 = smem_desc_sw128(base_addr, 8192, 1024);
+    const uint64_t dpt0 = smem_desc_sw128(smem_u32(pt_smem), 8192, 1024);
+    const uint64_t dvs = smem_desc_sw128(smem_u32(vs_smem), 8192, 1024);
+    constexpr uint64_t kStage = G::STAGE_BYTES >> 4, kQ = G::Q_BYTES >> 4;
     auto issue_mma1 = [&](int c) {
       const int s = c % STAGES;
       mbar_wait(&full[s], (c / STAGES) & 1);
       tc_fence_after();
-      const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
-      const uint32_t k_addr = q_addr + G::Q_BYTES;
+      const uint64_t dq = dq0 + s * kStage, dk = dq + kQ;
 #pragma unroll
       for (int kb = 0; kb < G::KB; ++kb)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_bf16_ss_elect(tbase + T_P, smem_desc_sw128(k_addr + kb * 8192 + kk * 32, 16, 1024),
-                            smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_qk, (kb | kk) != 0);
+          mma_bf16_ss_elect(tbase + T_P, dk + (kb * 512 + kk * 2), dq + (kb * 512 + kk * 2), id_qk,
+                            (kb | kk) != 0);
       mma_commit_elect(mma1_bar);
       V3_TRACE(5, c);
     };
     if (!state_only && nchunks > 0) issue_mma1(0);
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % STAGES;
-      const uint32_t q_addr = base_addr + s * G::STAGE_BYTES;
-      const uint32_t k_addr = q_addr + G::Q_BYTES;
-      const uint32_t v_addr = base_addr + G::OFF_V + (c % VST) * G::V_BYTES;
+      const uint64_t dq = dq0 + s * kStage;                               // Q, K-major
+      const uint64_t dk_mn = dmn0 + s * kStage + kQ;                      // K, MN-major (B of V'^T K)
+      const uint64_t dv_mn = dmn0 + ((G::OFF_V + (c % VST) * G::V_BYTES) >> 4);   // V, MN-major
       V3_TRACE(10, c);
       if (state_only) mbar_wait(&full[s], (c / STAGES) & 1);   // K_c landed (MMA1 waited otherwise)
       mbar_wait(&vs_bar[s], (c / STAGES) & 1);        // V'_c written
@@ -1250,8 +1253,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       tc_fence_after();
 #pragma unroll
       for (int ks = 0; ks < kC / 16; ++ks)
-        mma_bf16_ss_elect(tbase + T_S, smem_desc_sw128(vs_addr + ks * 2048, 8192, 1024),
-                          smem_desc_sw128(k_addr + ks * 2048, 8192, 1024), id_vk, 1);
+        mma_bf16_ss_elect(tbase + T_S, dvs + ks * 128, dk_mn + ks * 128, id_vk, 1);
       mma_commit_elect(mma_s_bar);
       V3_TRACE(3, c);
       if (!state_only) {
@@ -1263,19 +1265,18 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         for (int kb = 0; kb < G::KB; ++kb)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_bf16_ts_elect(tbase + T_O, tbase + T_SB + (kb * 4 + kk) * 8,
-                              smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq, (kb | kk) != 0);
+            mma_bf16_ts_elect(tbase + T_O, tbase + T_SB + (kb * 4 + kk) * 8, dq + (kb * 512 + kk * 2), id_sq,
+                              (kb | kk) != 0);
         mma_commit_elect(ox_bar);
         mma_commit_elect(&empty[s]);                  // Q_c, K_c consumed
         mbar_wait(&pt_bar[s], (c / STAGES) & 1);      // P^T_c in smem: its TMEM copy is free
         if (c + 1 < nchunks) issue_mma1(c + 1);
         mbar_wait(ox_scaled, c & 1);                  // O_inter(c) scaled by gamma^(t+1)
         tc_fence_after();
-        const uint32_t pt_addr_c = pt_addr + (c & 1) * G::PT_BYTES;
+        const uint64_t dpt = dpt0 + (c & 1) * (G::PT_BYTES >> 4);
 #pragma unroll
         for (int ks = 0; ks < kC / 16; ++ks)
-          mma_bf16_ss_elect(tbase + T_O, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
-                            smem_desc_sw128(pt_addr_c + ks * 2048, 8192, 1024), id_vp, 1);
+          mma_bf16_ss_elect(tbase + T_O, dv_mn + ks * 128, dpt + ks * 128, id_vp, 1);
         mma_commit_elect(mma_o_bar);
         V3_TRACE(4, c);
       } else {
