@@ -18,6 +18,7 @@
 // warps 4-7 epilogue-2 (outputs and state), warp 8 TMA producer, warp 9 MMA issuer
 // and TMEM owner.  Q/K/V chunks stream through an mbarrier ring of STAGES slots;
 // all operands are bf16 in 128B-swizzled shared memory; accumulators are fp32 in TMEM.
+#include <cstdlib>
 #include <mutex>
 #include <cudaTypedefs.h>
 
@@ -892,7 +893,11 @@ __device__ __forceinline__ void scale_row_blocks(const uint8_t* src, uint8_t* ds
 
 __device__ __forceinline__ uint32_t dup_lo(uint32_t w2) { return (w2 & 0xFFFFu) | (w2 << 16); }
 
-template <int DK, int STAGES>
+// MC = CTAs per cluster sharing each Q/K tile: the dv tiles of one head (blockIdx.x = cluster
+// rank).  Each CTA loads KB/MC of the 64-column Q/K boxes and multicasts them to all MC CTAs, so
+// L2 -> SM traffic for Q/K drops MC-fold; a stage is refilled only once every CTA released it
+// (tcgen05.commit multicast into each CTA's `empty`, arrival count MC).
+template <int DK, int STAGES, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -901,6 +906,8 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
                              const SegArgs sa, unsigned long long* __restrict__ trace) {
   using G = Cfg<DK, STAGES>;
   static_assert(DK % 128 == 0 && kDVT == 128, "layout: two state warps per TMEM subpartition");
+  static_assert(G::KB % MC == 0, "Q/K boxes split evenly over the cluster");
+  constexpr uint16_t kMask = (uint16_t)((1u << MC) - 1);
   constexpr int SCOL = DK / 2;                     // state columns per state warp
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -944,7 +951,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
   if (warp == 2 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], MC);
       mbar_init(&pt_bar[i], 64);
       mbar_init(&vs_bar[i], 64);
     }
@@ -970,8 +977,10 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
   if (warp == 3) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC > 1) cluster_sync_all();   // peers' barriers exist before any multicast
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  const uint32_t crank = MC > 1 ? cluster_ctarank() : 0;
   // debug: per-chunk clock64 of CTA (0,0,0), trace[event * 4096 + chunk]
   const bool tracing = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
 #define V3_TRACE(ev, c) do { if (tracing && lane == 0 && (c) < 4096) trace[(ev) * 4096 + (c)] = clock64(); } while (0)
@@ -1191,15 +1200,25 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES;
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % STAGES;
-        mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
+        mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);   // every CTA of the cluster released s
         V3_TRACE(9, c);
         uint8_t* st = smem + s * G::STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[s], bytes);
+        mbar_arrive_expect_tx(&full[s], bytes);        // the whole tile, from all MC issuers
 #pragma unroll
-        for (int kb = 0; kb < G::KB; ++kb) {
-          if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);
-          tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh);
+        for (int j = 0; j < G::KB / MC; ++j) {
+          const int kb = (int)crank * (G::KB / MC) + j;
+          if constexpr (MC > 1) {
+            if (!state_only) tma_load_3d_mc(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh, kMask);
+            tma_load_3d_mc(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh, kMask);
+          } else {
+            if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);
+            tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh);
+          }
         }
+      }
+      if constexpr (MC > 1) {   // peers' final releases have landed before this CTA may exit
+        for (int c = (nchunks > STAGES ? nchunks - STAGES : 0); c < nchunks; ++c)
+          mbar_wait(&empty[c % STAGES], (c / STAGES) & 1);
       }
     } else if (lane == 1) {
       for (int c = 0; c < nchunks; ++c) {
@@ -1268,7 +1287,8 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
             mma_bf16_ts_elect(tbase + T_O, tbase + T_SB + (kb * 4 + kk) * 8, dq + (kb * 512 + kk * 2), id_sq,
                               (kb | kk) != 0);
         mma_commit_elect(ox_bar);
-        mma_commit_elect(&empty[s]);                  // Q_c, K_c consumed
+        if constexpr (MC > 1) mma_commit_mc_elect(&empty[s], kMask);   // Q_c, K_c consumed (cluster)
+        else mma_commit_elect(&empty[s]);
         mbar_wait(&pt_bar[s], (c / STAGES) & 1);      // P^T_c in smem: its TMEM copy is free
         if (c + 1 < nchunks) issue_mma1(c + 1);
         mbar_wait(ox_scaled, c & 1);                  // O_inter(c) scaled by gamma^(t+1)
@@ -1280,7 +1300,8 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         mma_commit_elect(mma_o_bar);
         V3_TRACE(4, c);
       } else {
-        mma_commit_elect(&empty[s]);
+        if constexpr (MC > 1) mma_commit_mc_elect(&empty[s], kMask);
+        else mma_commit_elect(&empty[s]);
       }
       mma_commit_elect(&vempty[c % VST]);             // V_c consumed (O_intra / V')
     }
@@ -1288,6 +1309,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC > 1) cluster_sync_all();
   tc_fence_after();
   if (warp == 3) tmem_dealloc<kTmemCols>(tbase);
 }
@@ -1377,12 +1399,39 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   return cudaGetLastError();
 }
 
+template <int DK, int STAGES, int MC>
+cudaError_t launch_tmem_state_mc(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                                 const CUtensorMap& mo, const float* log2g, const float* s_in, float* s_out,
+                                 const ShapeArgs& s, bool state_only, const SegArgs& sa, int nz,
+                                 cudaStream_t stream) {
+  using G = v3::Cfg<DK, STAGES>;
+  static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
+  auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  if (err != cudaSuccess) return err;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)(s.B * s.H), (unsigned)nz);
+  cfg.blockDim = dim3(v3::kThreads);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = MC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  err = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H, (int)s.N, (int)s.dv,
+                           state_only ? 1 : 0, sa, g_trace);
+  count_launch();
+  if (err != cudaSuccess) return err;
+  return cudaGetLastError();
+}
+
 template <int DK, int STAGES>
 cudaError_t launch_tmem_state(const void* q, const void* k, const void* v, void* o, const float* log2g,
                               const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
                               const SegArgs& sa, int nz, cudaStream_t stream) {
-  using G = v3::Cfg<DK, STAGES>;
-  static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
   CUtensorMap mq, mk, mv;
   const int64_t BH = s.B * s.H;
   if (!make_map(&mk, k, s.dk, s.N, BH) || !make_map(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
@@ -1393,14 +1442,14 @@ cudaError_t launch_tmem_state(const void* q, const void* k, const void* v, void*
   }
   CUtensorMap mo = mk;
   if (!state_only && !make_map(&mo, o, s.dv, s.N, BH)) return cudaErrorInvalidValue;
-  auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-  if (err != cudaSuccess) return err;
-  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
-  kern<<<grid, v3::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H, (int)s.N,
-                                                (int)s.dv, state_only ? 1 : 0, sa, g_trace);
-  count_launch();
-  return cudaGetLastError();
+  // the dv tiles of a head share every Q/K tile: cluster them and multicast (LINATTN_NO_MULTICAST=1: off)
+  const int64_t tiles = (s.dv + kDVT - 1) / kDVT;
+  static const bool no_mc = getenv("LINATTN_NO_MULTICAST") != nullptr;
+  if (!no_mc && tiles == 4)
+    return launch_tmem_state_mc<DK, STAGES, 4>(mq, mk, mv, mo, log2g, s_in, s_out, s, state_only, sa, nz, stream);
+  if (!no_mc && tiles == 2)
+    return launch_tmem_state_mc<DK, STAGES, 2>(mq, mk, mv, mo, log2g, s_in, s_out, s, state_only, sa, nz, stream);
+  return launch_tmem_state_mc<DK, STAGES, 1>(mq, mk, mv, mo, log2g, s_in, s_out, s, state_only, sa, nz, stream);
 }
 
 }  // namespace
