@@ -169,3 +169,49 @@ def test_host_validation_errors_without_gpu():
         import ctypes
         lens = (ctypes.c_int64 * 2)(1, 2)
         _lib.check(lib.linattn_prefix_combine(1, 1, lens, 2, 5, 1, 1, 1, 4, 4, None))
+
+
+def test_bench_summarize_matches_reference_arithmetic():
+    """summarize() keeps the reference contract (reference tests/test_bench.py:20-36)."""
+    import math
+    import numpy as np
+    from paper_2501_02573_b200 import UsageError, summarize
+    mean, std = summarize([3, 1, 2, 9, 2], drop_extremes=True)
+    assert mean == pytest.approx(7 / 3) and std == pytest.approx(np.std([3, 2, 2], ddof=1))
+    assert summarize([2, 2, 2]) == (2, 0)
+    mean, std = summarize([1.0, 2.0, 3.0, 4.0])
+    assert mean == 2.5 and std == pytest.approx(math.sqrt(5 / 3))
+    with pytest.raises(UsageError):
+        summarize([1, 2], drop_extremes=True)
+
+
+def test_bench_gen_inputs_bitwise_reference_stream():
+    """gen_inputs draws the reference's PCG64 stream (bench.py:77-84) == the oracle's."""
+    import numpy as np
+    from oracle import linattn_oracle as orc
+    from paper_2501_02573_b200 import gen_inputs
+    a = gen_inputs(2, 3, 16, 4, 5, np.float32, seed=9, decay=True, gamma=0.7)
+    b, c, v = orc.gen_inputs(2, 3, 16, 4, 5, np.float32, 9)
+    assert np.array_equal(a.b, b) and np.array_equal(a.c, c) and np.array_equal(a.v, v)
+    assert a.gamma == [0.7] * 3 and a.decay
+    assert not np.array_equal(gen_inputs(2, 3, 16, 4, 5, np.float32, seed=10).b, a.b)
+
+
+def test_bench_render_and_usage_errors():
+    from paper_2501_02573_b200 import BenchConfig, MethodId, UsageError, render_report, run_bench
+    from paper_2501_02573_b200.bench import BenchReport, BenchRow
+    row = BenchRow(MethodId.B200_CHUNKED, 1, 2, 64, 8, 8, "decay", 0.9, "bf16", 1e-4, 1e-6, 123, "ok",
+                   100.0, 0.5, 1.0)
+    oom = BenchRow(MethodId.B200_CHUNKED_F32, 1, 2, 64, 8, 8, "decay", 0.9, "f32", None, None, None, "OOM")
+    rep = BenchReport(rows=[row, oom], meta={"seed": 0})
+    csv = render_report(rep, "csv").splitlines()
+    assert csv[0].startswith("method,batch,heads,seqlen") and csv[0].endswith("gbps,frac_hbm,tflops_c64")
+    assert csv[1].startswith("b200-chunked,1,2,64,8,8,decay,0.9,bf16,0.0001,") and csv[2].endswith("OOM,,,")
+    md = render_report(rep, "markdown")
+    assert "| b200-chunked |" in md and "OOM" in md and "50% HBM" in md
+    with pytest.raises(UsageError):
+        render_report(rep, "xml")
+    with pytest.raises(UsageError):
+        run_bench(BenchConfig(methods=[MethodId.AUTO], grid=[(1, 1, 8, 2, 2)]))
+    with pytest.raises(UsageError):
+        run_bench(BenchConfig(methods=[MethodId.B200_CHUNKED], grid=[]))

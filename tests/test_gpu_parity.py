@@ -305,3 +305,15 @@ def test_split_binary_mask_and_partial_dv_tile(la, dk, dv, decay):
     out = ops.prefill(dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16),
                       ops.log2_gamma(gam, decay, "cuda"))
     assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
+
+
+def test_run_bench_gpu_rows(la):
+    """run_bench with CUDA-event timing and roofline columns (reference bench.py:87-125)."""
+    cfg = la.BenchConfig(methods=[la.MethodId.B200_CHUNKED, la.MethodId.B200_CHUNKED_F32],
+                         grid=[(1, 4, 1024, 64, 64), (2, 2, 333, 128, 128)], decay=True, repeats=3, warmup=1)
+    rep = la.run_bench(cfg)
+    assert len(rep.rows) == 4
+    for r in rep.rows:
+        assert r.status == "ok" and r.mean_s > 0 and r.opcount > 0 and r.gbps > 0 and 0 < r.frac_hbm < 1.5
+    assert "PCG64" in rep.meta["generator"] and "CUDA events" in rep.meta["timing"]
+    assert la.render_report(rep, "csv").count("\n") == 5
