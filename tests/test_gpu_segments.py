@@ -129,3 +129,39 @@ def test_split_causality_and_linearity(ops):
     ref, _ = orc.seeded_blocked_attn(qq[None, None, N - 4096:], kk[None, None, N - 4096:],
                                      vv[None, None, N - 4096:], [gam[h]], True, s_pre[None, None], block=64)
     assert orc.max_rel_error(o[0, h, N - 4096:].float().cpu().numpy(), ref[0, 0]) <= TOL_BF16
+
+
+def test_cuda_graph_capture_split_and_decode(ops):
+    """The split prefill (stream-ordered pool workspace) and the decode step replay from a CUDA graph."""
+    torch.manual_seed(2)
+    B, H, N, d = 1, 4, 8192, 128
+    q = torch.randn(B, H, N, d, device="cuda", dtype=torch.bfloat16)
+    k, v = torch.randn_like(q), torch.randn_like(q)
+    l2 = ops.log2_gamma([0.99, 0.999, 0.5, 1.0], True, "cuda")
+    assert ops.seq_plan(B, H, N, d, d)[1] > 1
+    out = torch.empty_like(v)
+    st = torch.zeros(B, H, d, d, device="cuda")
+    qd, kd, vd = (x[:, :, 0].contiguous() for x in (q, k, v))
+    od = torch.empty_like(vd)
+    want = ops.prefill(q, k, v, l2).clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        ops.prefill(q, k, v, l2, out=out)          # warm-up outside capture
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            ops.prefill(q, k, v, l2, out=out)
+            ops.decode_step(qd, kd, vd, st, l2, out=od)
+    torch.cuda.current_stream().wait_stream(s)
+    out.zero_()
+    st.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
+    # two replays of the decode step from S = 0: S = (gamma + 1) k^T v
+    s2 = torch.zeros_like(st)
+    ops.decode_step(qd, kd, vd, s2, l2)
+    ops.decode_step(qd, kd, vd, s2, l2)
+    assert torch.allclose(st, s2, rtol=1e-6, atol=1e-6)

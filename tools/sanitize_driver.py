@@ -1,0 +1,24 @@
+"""Small launches of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2501_02573_b200 import ops  # noqa: E402
+
+torch.manual_seed(0)
+for (B, H, N, dk, dv) in [(1, 2, 300, 128, 128), (1, 1, 200, 64, 64), (1, 1, 130, 256, 512)]:
+    q = torch.randn(B, H, N, dk, device="cuda", dtype=torch.bfloat16)
+    k = torch.randn_like(q)
+    v = torch.randn(B, H, N, dv, device="cuda", dtype=torch.bfloat16)
+    l2 = ops.log2_gamma([0.9] * H, True, "cuda")
+    s_out = torch.empty(B, H, dk, dv, device="cuda")
+    ops.prefill(q, k, v, l2, s_out=s_out)                      # tensor-core kernel
+    ops.prefill(q, k, v, l2, seq_split=3)                      # split: state pass + seeded segments
+    ops.prefill(q.float(), k.float(), v.float(), l2, kernel="simt")
+    st = torch.zeros(B, H, dk, dv, device="cuda")
+    ops.decode_step(q[:, :, 0].contiguous(), k[:, :, 0].contiguous(), v[:, :, 0].contiguous(), st, l2)
+    ops.prefix_combine(torch.stack([s_out, s_out]), [N, N], 1, l2)
+torch.cuda.synchronize()
+print("sanitize driver done")
