@@ -165,3 +165,31 @@ def test_cuda_graph_capture_split_and_decode(ops):
     ops.decode_step(qd, kd, vd, s2, l2)
     ops.decode_step(qd, kd, vd, s2, l2)
     assert torch.allclose(st, s2, rtol=1e-6, atol=1e-6)
+
+
+def test_long_context_gamma_near_one(ops):
+    """SURVEY.md 7 "decay numerics": gamma in [1-1e-5, 1-1e-7] at N = 131072 (configs[4] length).
+
+    fp32-rounded gamma would put ~4e-3 relative error on gamma^n there; the kernels take log2(gamma)
+    derived in f64.  The split prefill's last 2048 tokens are checked against an f64 reference
+    seeded with the exact f64 prefix state.
+    """
+    torch.manual_seed(3)
+    B, H, N, d = 1, 2, 131072, 64
+    gam = [1 - 1e-5, 1 - 1e-7]
+    q = (torch.randn(B, H, N, d, device="cuda") * 0.25).to(torch.bfloat16)
+    k = (torch.randn(B, H, N, d, device="cuda") * 0.25).to(torch.bfloat16)
+    v = torch.randn(B, H, N, d, device="cuda").to(torch.bfloat16)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    assert ops.seq_plan(B, H, N, d, d)[1] > 1
+    o = ops.prefill(q, k, v, l2)
+    T = 2048
+    for h in range(H):
+        kk = k[0, h].double().cpu().numpy()
+        vv = v[0, h].double().cpu().numpy()
+        w = np.exp((N - T - 1 - np.arange(N - T)) * np.log(gam[h]))        # f64 gamma^(L-1-t)
+        s_pre = (kk[:N - T] * w[:, None]).T @ vv[:N - T]
+        qq = q[0, h, N - T:].double().cpu().numpy()
+        ref, _ = orc.seeded_blocked_attn(qq[None, None], kk[None, None, N - T:], vv[None, None, N - T:],
+                                         [gam[h]], True, s_pre[None, None], block=64)
+        assert orc.max_rel_error(o[0, h, N - T:].float().cpu().numpy(), ref[0, 0]) <= TOL_BF16
