@@ -385,6 +385,10 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
 namespace v2 {
 
 constexpr int kThreads = 448;
+#ifndef V2_OT_BUFS
+#define V2_OT_BUFS 1
+#endif
+constexpr int kOtBufs = V2_OT_BUFS;     // output staging tiles (2: a store never blocks the next chunk)
 #ifndef LA_L2_AHEAD
 #define LA_L2_AHEAD 0
 #endif
@@ -405,7 +409,9 @@ struct Cfg {
   static constexpr int OT_BYTES = kC * kDVT * 2;    // one output staging tile [64 t][128 d]
   static constexpr int OFF_PT = STAGES * STAGE_BYTES;
   static constexpr int OFF_OT = OFF_PT + 2 * PT_BYTES;
-  static constexpr int OFF_POW = OFF_OT + OT_BYTES;           // fp32 gamma^n, n = 0..64
+  static constexpr int OT_BUFS =                               // double-buffer the output tile if it fits
+      (OFF_OT + kOtBufs * OT_BYTES + 128 * 4 + 192 * 4 + 512 + 1024 <= 227 * 1024) ? kOtBufs : 1;
+  static constexpr int OFF_POW = OFF_OT + OT_BUFS * OT_BYTES; // fp32 gamma^n, n = 0..64
   static constexpr int OFF_POW2 = OFF_POW + 128 * 4;          // bf16x2 (gamma^k, gamma^(k+1)), k = -64..127
   static constexpr int OFF_BAR = OFF_POW2 + 192 * 4;
   static constexpr int SMEM = OFF_BAR + 512 + 1024;
@@ -492,7 +498,9 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const bool tracing = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
+  // debug trace of one CTA: (bh = trace[15 * 4096], dv tile 0, segment 0); trace[15 * 4096] is set by the host
+  const bool tracing = trace != nullptr && blockIdx.x == 0 && blockIdx.z == 0 &&
+                       blockIdx.y == (unsigned)trace[15 * 4096];
   const int lin_block = blockIdx.y * gridDim.x + blockIdx.x;
   auto gtime = [] {
     unsigned long long t;
@@ -659,8 +667,8 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       tc_fence_after();
       // ---- outputs of chunk c: O = Oi + gamma^(t+1) Ox (16 lanes x 64 tokens) -> bf16 ->
       //      smem [t][d] (stmatrix.trans, 128B swizzle) -> TMA bulk store (clips N and dv)
-      uint8_t* ot = ot_smem;
-      if (leader) bulk_wait_read<0>();           // the previous chunk's store has read the tile
+      uint8_t* ot = ot_smem + (c % G::OT_BUFS) * G::OT_BYTES;
+      if (leader) bulk_wait_read<G::OT_BUFS - 1>();   // the store that last used this tile has read it
       named_bar_sync(1, 256);
 #pragma unroll
       for (int q4 = 0; q4 < 2; ++q4) {           // tokens q4*32 .. q4*32+31
@@ -1456,6 +1464,10 @@ cudaError_t launch_tmem_state(const void* q, const void* k, const void* v, void*
 
 void set_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
 
+#ifndef V2_STAGES128
+#define V2_STAGES128 4
+#endif
+
 bool tc_supported(const ShapeArgs& s, int dtype) {
   if (dtype != LINATTN_BF16) return false;
   if (!(s.dk == 64 || s.dk == 128 || s.dk == 256)) return false;
@@ -1471,7 +1483,7 @@ cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void*
     if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return cudaErrorNotSupported;
   switch (s.dk) {
     case 64: return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
-    case 128: return launch_pipe<128, 4>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
+    case 128: return launch_pipe<128, V2_STAGES128>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
     case 256: return launch_tmem_state<256, 2>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
     default: return cudaErrorNotSupported;
   }

@@ -9,10 +9,11 @@ EV = ["-", "dS_issue", "O_issue", "P_done", "K_done", "O_stored", "dS_loaded", "
       "mma1_full_ok", "mma1_issued", "epi1_ok", "tma_load_issue", "st_full_ok", "-"]
 
 
-def main(mode="full", B=8, H=32, N=8192, d=128):
+def main(mode="full", B=8, H=32, N=8192, d=128, cta=0):
     lib = _lib.load()
     lib.linattn_debug_set_trace.argtypes = [ctypes.c_void_p]
     buf = torch.zeros(16 * 4096, dtype=torch.int64, device="cuda")
+    buf[15 * 4096] = int(cta)   # which (b*h) CTA to trace
     q = torch.randn(B, H, N, d, device="cuda", dtype=torch.bfloat16)
     k, v = torch.randn_like(q), torch.randn_like(q)
     l2 = ops.log2_gamma([0.99] * H, True, "cuda")
@@ -52,4 +53,4 @@ def main(mode="full", B=8, H=32, N=8192, d=128):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["full"]))
+    main(sys.argv[1] if len(sys.argv) > 1 else "full", cta=int(sys.argv[2]) if len(sys.argv) > 2 else 0)
