@@ -2,6 +2,7 @@
 // Host-side validation mirrors the reference's typed errors (tensor.py:97-123,
 // errors.py:4-29); every entry point is stream-ordered and never synchronises.
 #include <algorithm>
+#include <initializer_list>
 #include <cstdio>
 #include <cstdarg>
 #include <atomic>
@@ -47,6 +48,12 @@ static int check_dims(const ShapeArgs& s, bool need_n) {
 }
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static bool aligned16(std::initializer_list<const void*> ptrs) {
+  for (const void* p : ptrs)
+    if (reinterpret_cast<uintptr_t>(p) & 15) return false;
+  return true;
+}
 static int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 static int sm_count() {
@@ -156,11 +163,12 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
   if (int e = check_dtype(dtype)) return e;
   if (!q || !k || !v || !o || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
   cudaStream_t st = (cudaStream_t)stream;
-  const bool tc_ok = tc_supported(s, dtype);
+  // TMA needs 16-byte aligned bases; AUTO routes an unaligned view to the FFMA kernel
+  const bool tc_ok = tc_supported(s, dtype) && aligned16({q, k, v, o});
   if (kernel == LINATTN_KERNEL_TC && !tc_ok)
     return fail(LINATTN_EUNSUPPORTED,
-                "tensor-core prefill needs bf16, dk in {64,128,256} and dv %% 64 == 0 "
-                "(got dtype=%d dk=%lld dv=%lld)", dtype, (long long)dk, (long long)dv);
+                "tensor-core prefill needs bf16, dk in {64,128,256}, dv %% 64 == 0 and 16-byte aligned "
+                "tensors (got dtype=%d dk=%lld dv=%lld)", dtype, (long long)dk, (long long)dv);
   if (kernel != LINATTN_KERNEL_AUTO && kernel != LINATTN_KERNEL_TC && kernel != LINATTN_KERNEL_SIMT)
     return fail(LINATTN_EPARAM, "unknown kernel selector %d", kernel);
   if (kernel != LINATTN_KERNEL_SIMT && tc_ok) {
@@ -200,9 +208,9 @@ int linattn_state_pass(const void* k, const void* v, float* s_out, const float* 
   if (int e = check_dtype(dtype)) return e;
   if (!k || !v || !s_out || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
   cudaStream_t st = (cudaStream_t)stream;
-  const bool tc_ok = tc_supported(s, dtype);
+  const bool tc_ok = tc_supported(s, dtype) && aligned16({k, v});
   if (kernel == LINATTN_KERNEL_TC && !tc_ok)
-    return fail(LINATTN_EUNSUPPORTED, "tensor-core state pass needs bf16 and a supported shape");
+    return fail(LINATTN_EUNSUPPORTED, "tensor-core state pass needs bf16, a supported shape and aligned tensors");
   if (kernel != LINATTN_KERNEL_SIMT && tc_ok)
     return cuda_status(launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, s_out, s, true,
                                          SegArgs{}, 1, st), "state_pass_tc");
@@ -241,9 +249,9 @@ int linattn_state_pass_segmented(const void* k, const void* v, float* loc_out, c
   if (int e = check_dims(s, true)) return e;
   if (int e = check_dtype(dtype)) return e;
   if (!k || !v || !loc_out || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
-  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype);
+  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype) && aligned16({k, v});
   if (kernel == LINATTN_KERNEL_TC && !tc)
-    return fail(LINATTN_EUNSUPPORTED, "tensor-core state pass needs bf16 and a supported shape");
+    return fail(LINATTN_EUNSUPPORTED, "tensor-core state pass needs bf16, a supported shape and aligned tensors");
   if (int e = check_seg(s, seg_len, m, tc)) return e;
   if (nseg < 1 || nseg > ceil_div(N, seg_len) || nseg * m > 65535)
     return fail(LINATTN_EPARAM, "segment count %lld outside [1, ceil(N/seg_len)=%lld]", (long long)nseg,
@@ -265,9 +273,9 @@ int linattn_prefill_segmented(const void* q, const void* k, const void* v, void*
   if (int e = check_dims(s, true)) return e;
   if (int e = check_dtype(dtype)) return e;
   if (!q || !k || !v || !o || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
-  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype);
+  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype) && aligned16({q, k, v, o});
   if (kernel == LINATTN_KERNEL_TC && !tc)
-    return fail(LINATTN_EUNSUPPORTED, "tensor-core prefill needs bf16, dk in {64,128,256}, dv %% 64 == 0");
+    return fail(LINATTN_EUNSUPPORTED, "tensor-core prefill needs bf16, dk in {64,128,256}, dv %% 64 == 0, aligned");
   if (int e = check_seg(s, seg_len, 1, tc)) return e;
   if (loc && (nloc < 0 || loc_seg_len < 1 || loc_m < 1 || nloc > ceil_div(N, loc_seg_len) * loc_m))
     return fail(LINATTN_EPARAM, "bad local-state geometry (seg_len %lld, m %lld, count %lld)",

@@ -317,3 +317,27 @@ def test_run_bench_gpu_rows(la):
         assert r.status == "ok" and r.mean_s > 0 and r.opcount > 0 and r.gbps > 0 and 0 < r.frac_hbm < 1.5
     assert "PCG64" in rep.meta["generator"] and "CUDA events" in rep.meta["timing"]
     assert la.render_report(rep, "csv").count("\n") == 5
+
+
+def test_unaligned_views_route_to_ffma_kernel(la):
+    """A contiguous but 2-byte-offset view cannot be a TMA base: AUTO runs the FFMA kernel,
+    an explicit tensor-core request raises the reference's UsageError."""
+    from paper_2501_02573_b200 import ops
+    B, H, N, d = 1, 2, 200, 64
+    b, c, v = (orc.bf16_round(x) for x in orc.gen_inputs(B, H, N, d, d, np.float32, 17))
+    gam = [0.9, 0.99]
+    ref = orc.oracle_attn(b, c, v, gam, True)
+
+    def unaligned(x):
+        flat = torch.empty(x.size + 1, device="cuda", dtype=torch.bfloat16)
+        view = flat[1:].view(x.shape)
+        view.copy_(torch.from_numpy(x))
+        assert view.data_ptr() % 16 != 0
+        return view
+
+    q, k, vv = unaligned(b), unaligned(c), unaligned(v)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    out = ops.prefill(q, k, vv, l2)
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
+    with pytest.raises(la.UsageError):
+        ops.prefill(q, k, vv, l2, kernel="tc")
