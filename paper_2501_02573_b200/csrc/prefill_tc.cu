@@ -901,6 +901,29 @@ __device__ __forceinline__ void scale_row_blocks(const uint8_t* src, uint8_t* ds
 
 __device__ __forceinline__ uint32_t dup_lo(uint32_t w2) { return (w2 & 0xFFFFu) | (w2 << 16); }
 
+// Lazy decay normalisation.  gamma is a per-head SCALAR, so the state is kept as S_c = sig_c T_c:
+// the update S_{c+1} = gamma^L S_c + V'^T K becomes T_{c+1} = T_c + (V'/sig_{c+1})^T K with
+// sig_{c+1} = sig_c gamma^L -- the 1/sig factor rides on V' (16 KiB, already rescaled every
+// chunk) and sig_c on the O_inter column scale, so the 128 KiB TMEM state is not rewritten.
+// When sig would drop below kSigMin (or gamma^L itself is tiny, e.g. gamma = 0) the chunk
+// renormalises: T <- sig gamma^L T in TMEM and sig = 1.  Every role walks the same sequence.
+constexpr float kSigMin = 0x1p-40f;
+struct Lazy {
+  float sig = 1.f;      // sig_c of the chunk about to be processed
+  float sig_c = 1.f;    // sig_c saved for this chunk's O_inter scale
+  float vfac = 1.f;     // factor on V'_c (1 / sig_{c+1}, or 1 when renormalising)
+  float rescale = 1.f;  // T_c multiplier when renormalising
+  bool renorm = false;
+  __device__ __forceinline__ void step(float gL) {
+    sig_c = sig;
+    const float sn = sig * gL;
+    renorm = !(sn >= kSigMin);
+    rescale = sn;
+    vfac = renorm ? 1.f : 1.f / sn;
+    sig = renorm ? 1.f : sn;
+  }
+};
+
 // MC = CTAs per cluster sharing each Q/K tile: the dv tiles of one head (blockIdx.x = cluster
 // rank).  Each CTA loads KB/MC of the 64-column Q/K boxes and multicasts them to all MC CTAs, so
 // L2 -> SM traffic for Q/K drops MC-fold; a stage is refilled only once every CTA released it
@@ -994,8 +1017,9 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
 #define V3_TRACE(ev, c) do { if (tracing && lane == 0 && (c) < 4096) trace[(ev) * 4096 + (c)] = clock64(); } while (0)
 
   if (warp < 2) {
-    // ------------------------------------------------------------ P^T mask (TMEM lanes 0-63)
+    // ------------------------------------------------------------ V' and P^T mask (TMEM lanes 0-63)
     const int srow = warp * 32 + lane;
+    Lazy lz;
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % STAGES;
       const int L = min(kC, hi - lo - c * kC);
@@ -1005,9 +1029,10 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         tc_fence_after();
       }
       if (warp == 0) V3_TRACE(12, c);
-      {   // V'[s] = gamma^(L-1-s) V[s], 0 past L (row srow, both 64-column blocks)
-        const uint32_t w2 = pw2[srow < L ? L - 1 - srow : -64];
-        scale_row_blocks<kDVT / 64>(smem + G::OFF_V + (c % VST) * G::V_BYTES, vs_smem, srow, 0, dup_lo(w2));
+      lz.step(pw[L]);
+      {   // V'[s] = gamma^(L-1-s) V[s] / sig_{c+1}, 0 past L (row srow, both 64-column blocks)
+        const float w = srow < L ? pw[L - 1 - srow] * lz.vfac : 0.f;
+        scale_row_blocks<kDVT / 64>(smem + G::OFF_V + (c % VST) * G::V_BYTES, vs_smem, srow, 0, pack_bf16x2(w, w));
       }
       fence_proxy_async_smem();
       mbar_arrive(&vs_bar[s]);
@@ -1093,15 +1118,16 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         bulk_commit();
       }
     };
+    Lazy lz;
     for (int c = 0; c < (state_only ? 0 : nchunks); ++c) {
       const int s = c % STAGES;
       const int L = min(kC, hi - lo - c * kC);
       uint8_t* stage = smem + s * G::STAGE_BYTES;
-      (void)L;
       (void)stage;
       (void)s;
+      lz.step(pw[L]);
       {
-        // O_inter(c)[d][t] *= gamma^(t+1)  (fp32, in TMEM: lanes sub*32.., columns t)
+        // O_inter(c)[d][t] *= sig_c gamma^(t+1)  (fp32, in TMEM: lanes sub*32.., columns t)
         mbar_wait(ox_bar, c & 1);
         tc_fence_after();
         const uint32_t ta_o = tbase + ((uint32_t)(sub * 32) << 16) + T_O;
@@ -1111,7 +1137,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
           tmem_ld32(ta_o + half * 32, o);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] *= pw[half * 32 + i + 1];
+          for (int i = 0; i < 32; ++i) o[i] *= lz.sig_c * pw[half * 32 + i + 1];
           tmem_st32(ta_o + half * 32, o);
         }
         tmem_wait_st();
@@ -1160,6 +1186,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       }
       tmem_wait_st();
     }
+    Lazy lz;
     for (int c = 0; c < nchunks; ++c) {
       const int L = min(kC, hi - lo - c * kC);
       if (c > 0) {
@@ -1169,23 +1196,28 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         tc_fence_after();
       }
       if (warp == 4) V3_TRACE(0, c);
-      const float carry = pw[L];
+      lz.step(pw[L]);
+      // publish bf16 T_c for O_inter(c); rewrite T only when renormalising (T <- sig gamma^L T)
+      if (!state_only || lz.renorm) {
 #pragma unroll 1
-      for (int cb = 0; cb < SCOL / 32; ++cb) {
-        float sv[32];
-        tmem_ld32(ta_s + cb * 32, sv);
-        tmem_wait_ld();
-        if (!state_only) {
-          uint32_t pk[16];
+        for (int cb = 0; cb < SCOL / 32; ++cb) {
+          float sv[32];
+          tmem_ld32(ta_s + cb * 32, sv);
+          tmem_wait_ld();
+          if (!state_only) {
+            uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(sv[2 * i], sv[2 * i + 1]);
-          tmem_st16(ta_sb + cb * 16, pk);
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(sv[2 * i], sv[2 * i + 1]);
+            tmem_st16(ta_sb + cb * 16, pk);
+          }
+          if (lz.renorm) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sv[i] *= lz.rescale;
+            tmem_st32(ta_s + cb * 32, sv);
+          }
         }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) sv[i] *= carry;
-        tmem_st32(ta_s + cb * 32, sv);
+        tmem_wait_st();
       }
-      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(st_done);
       if (warp == 4) V3_TRACE(1, c);
@@ -1198,7 +1230,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         tmem_ld32(ta_s + cb * 32, sv);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = sv[i];
+        for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = lz.sig * sv[i];   // S = sig T
       }
     }
   } else if (warp == 2) {

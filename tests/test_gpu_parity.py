@@ -341,3 +341,20 @@ def test_unaligned_views_route_to_ffma_kernel(la):
     assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
     with pytest.raises(la.UsageError):
         ops.prefill(q, k, vv, l2, kernel="tc")
+
+
+@pytest.mark.parametrize("decay", [True, False])
+def test_dk256_lazy_normalisation_regimes(la, decay):
+    """dk=256 keeps S = sig * T with a scalar sig per head; gamma = 0.5 renormalises every chunk,
+    0.9 every few chunks, 0.99 / 0.9999 rarely or never, 0 always, 1 never (binary mask)."""
+    from paper_2501_02573_b200 import ops
+    gam = [0.5, 0.9, 0.99, 0.9999, 0.0, 1.0]
+    b, c, v = (orc.bf16_round(x) for x in orc.gen_inputs(1, 6, 3000, 256, 256, np.float32, 19))
+    v = orc.bf16_round(v * 0.25)
+    ref = orc.oracle_attn(b, c, v, gam if decay else [1.0] * 6, decay)
+    s_out = torch.empty(1, 6, 256, 256, device="cuda")
+    out = ops.prefill(dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16),
+                      ops.log2_gamma(gam, decay, "cuda"), s_out=s_out, seq_split=1)
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
+    ref_s = np.stack([[orc.segment_end_state(c[0, h], v[0, h], gam[h] if decay else 1.0) for h in range(6)]])
+    assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= 5e-3
