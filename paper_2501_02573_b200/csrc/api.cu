@@ -111,16 +111,17 @@ static void attach_loc(SegArgs& a, const float* loc, int64_t loc_seg_len, int64_
 // Sequence-split plan for one device: when batch x head x dv-tiles
 // leaves SMs idle, cut the sequence into nseg segments so nseg * units fills one wave; the
 // state-only pass over the first nseg-1 segments is split m more ways to fill its own wave.
+// Tensor-core kernel: 128-wide dv tiles, one CTA per SM (it owns all 512 TMEM columns).
+// FFMA kernel (fp32 parity mode, compute-bound): 64-wide dv tiles, two CTAs per SM.
 struct Plan {
   int64_t seg_len, nseg, m;
 };
 
-static Plan plan_split(const ShapeArgs& s, int dtype, int kernel) {
+static Plan plan_split(const ShapeArgs& s, bool tc) {
   Plan p{s.N, 1, 1};
-  if (kernel == LINATTN_KERNEL_SIMT || !tc_supported(s, dtype)) return p;
-  const int64_t sms = sm_count();
-  const int64_t units = s.B * s.H * ceil_div(s.dv, 128);
-  int64_t nseg = std::min<int64_t>(sms / std::max<int64_t>(units, 1), s.N / 512);
+  const int64_t slots = sm_count() * (tc ? 1 : 2);
+  const int64_t units = s.B * s.H * ceil_div(s.dv, tc ? 128 : 64);
+  int64_t nseg = std::min<int64_t>(slots / std::max<int64_t>(units, 1), s.N / (tc ? 512 : 256));
   if (nseg < 2) return p;
   const int64_t seg = round_up(ceil_div(s.N, nseg), 64);
   nseg = ceil_div(s.N, seg);
@@ -131,7 +132,7 @@ static Plan plan_split(const ShapeArgs& s, int dtype, int kernel) {
   for (int64_t m = 1; m <= 8; ++m) {
     if (sub_len(seg, m) < 256) break;
     const int64_t ctas = ua * m;
-    const double eff = (double)ctas / (double)(ceil_div(ctas, sms) * sms);
+    const double eff = (double)ctas / (double)(ceil_div(ctas, slots) * slots);
     if (eff > best + 0.02) {
       best = eff;
       best_m = m;
@@ -171,33 +172,34 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
                 "tensors (got dtype=%d dk=%lld dv=%lld)", dtype, (long long)dk, (long long)dv);
   if (kernel != LINATTN_KERNEL_AUTO && kernel != LINATTN_KERNEL_TC && kernel != LINATTN_KERNEL_SIMT)
     return fail(LINATTN_EPARAM, "unknown kernel selector %d", kernel);
-  if (kernel != LINATTN_KERNEL_SIMT && tc_ok) {
-    const Plan pl = plan_split(s, dtype, kernel);
-    if (pl.nseg > 1) {
-      // two-phase split: local states of segments 0..nseg-2 (m-way sub-split), then every
-      // segment seeded from them in its prologue; workspace from the library's stream pool
-      const int64_t nloc = (pl.nseg - 1) * pl.m;
-      const size_t bytes = (size_t)nloc * s.B * s.H * s.dk * s.dv * sizeof(float);
-      float* loc = nullptr;
-      cudaMemPool_t pool = work_pool();
-      if (pool && cudaMallocFromPoolAsync((void**)&loc, bytes, pool, st) == cudaSuccess) {
-        SegArgs a = make_seg(pl.seg_len, pl.m);
-        cudaError_t e = launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, loc, s, true, a, (int)nloc, st);
-        if (e == cudaSuccess) {
-          SegArgs b = make_seg(pl.seg_len, 1);
-          attach_loc(b, loc, pl.seg_len, pl.m, nloc);
-          e = launch_prefill_tc(q, k, v, o, log2g, s_in, s_out, s, false, b, (int)pl.nseg, st);
-        }
-        cudaFreeAsync(loc, st);
-        return cuda_status(e, "prefill_tc (sequence split)");
+  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_ok;
+  auto launch = [&](const void* q_, const void* o_, const float* si, float* so, bool state_only,
+                    const SegArgs& a, int nz) {
+    return tc ? launch_prefill_tc(q_, k, v, (void*)o_, log2g, si, so, s, state_only, a, nz, st)
+              : launch_prefill_simt(q_, k, v, (void*)o_, log2g, si, so, s, dtype, state_only, a, nz, st);
+  };
+  const char* what = tc ? "prefill_tc" : "prefill_simt";
+  const Plan pl = plan_split(s, tc);
+  if (pl.nseg > 1) {
+    // two-phase split: local states of segments 0..nseg-2 (m-way sub-split), then every
+    // segment seeded from them in its prologue; workspace from the library's stream pool
+    const int64_t nloc = (pl.nseg - 1) * pl.m;
+    const size_t bytes = (size_t)nloc * s.B * s.H * s.dk * s.dv * sizeof(float);
+    float* loc = nullptr;
+    cudaMemPool_t pool = work_pool();
+    if (pool && cudaMallocFromPoolAsync((void**)&loc, bytes, pool, st) == cudaSuccess) {
+      cudaError_t e = launch(nullptr, nullptr, nullptr, loc, true, make_seg(pl.seg_len, pl.m), (int)nloc);
+      if (e == cudaSuccess) {
+        SegArgs b = make_seg(pl.seg_len, 1);
+        attach_loc(b, loc, pl.seg_len, pl.m, nloc);
+        e = launch(q, o, s_in, s_out, false, b, (int)pl.nseg);
       }
-      cudaGetLastError();  // no workspace: run unsplit
+      cudaFreeAsync(loc, st);
+      return cuda_status(e, tc ? "prefill_tc (sequence split)" : "prefill_simt (sequence split)");
     }
-    return cuda_status(launch_prefill_tc(q, k, v, o, log2g, s_in, s_out, s, false, SegArgs{}, 1, st),
-                       "prefill_tc");
+    cudaGetLastError();  // no workspace: run unsplit
   }
-  return cuda_status(launch_prefill_simt(q, k, v, o, log2g, s_in, s_out, s, dtype, false, SegArgs{}, 1, st),
-                     "prefill_simt");
+  return cuda_status(launch(q, o, s_in, s_out, false, SegArgs{}, 1), what);
 }
 
 int linattn_state_pass(const void* k, const void* v, float* s_out, const float* log2g, int64_t B,
@@ -234,7 +236,7 @@ int linattn_seq_plan(int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv, in
   if (int e = check_dims(s, true)) return e;
   if (int e = check_dtype(dtype)) return e;
   if (!plan) return fail(LINATTN_EPARAM, "null plan pointer");
-  const Plan p = plan_split(s, dtype, kernel);
+  const Plan p = plan_split(s, kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype));
   plan[0] = p.seg_len;
   plan[1] = p.nseg;
   plan[2] = p.m;

@@ -41,7 +41,9 @@ def test_seq_plan_shapes(ops):
     seg, nseg, m, sub = ops.seq_plan(1, 32, 131072, 128, 128)        # configs[4] on one GPU
     assert nseg > 1 and seg % 64 == 0 and nseg * 32 <= sms and sub % 64 == 0
     assert ops.seq_plan(8, 32, 8192, 128, 128)[1] == 1                # configs[1]: units fill the SMs
-    assert ops.seq_plan(1, 1, 4096, 128, 128, torch.float32)[1] == 1  # fp32 parity mode never splits
+    # fp32 parity mode (FFMA kernel, 64-wide dv tiles, 2 CTAs/SM) splits too: configs[0] shape
+    seg, nseg, m, _ = ops.seq_plan(1, 8, 2048, 64, 64, torch.float32)
+    assert nseg > 1 and 8 * nseg <= 2 * sms and seg % 64 == 0
 
 
 @pytest.mark.parametrize("dk,dv", [(128, 128), (64, 128), (256, 256)])
