@@ -1,23 +1,21 @@
 // K1 (+K2, K4): tensor-core chunked prefill for sm_100a -- TMA + tcgen05 + TMEM.
 //
-// One CTA owns one (batch*head, 128-wide dv tile) unit and walks its sequence in
-// chunks of C = 64 tokens.  The algebra is the reference two-level-block method
-// (kernels.py:139-166) written TRANSPOSED so every accumulator has M = 128 TMEM
-// lanes (lane = dv row) and the chunk can stay at the reference's C = 64:
+// One CTA owns one (batch*head, 128-wide dv tile, sequence segment) unit and walks its tokens in
+// chunks of C = 64 (the reference default, kernels.py:57).  The algebra is the reference
+// two-level-block method (kernels.py:139-166) written TRANSPOSED so every accumulator has
+// M = 128 TMEM lanes (lane = dv row) while the chunk stays at 64:
 //
 //   MMA1  P^T[s][t]   = sum_i K[s][i] Q[t][i]              (M=128 (64 live), N=64, K=dk)
 //   epi1  P^T[s][t]  *= gamma^(t-s) for t >= s else 0      (mask built from a gamma^n table)
-//         K'[s]       = gamma^(L-1-s) K[s]                 (in place, smem)
 //   MMA2  Oi^T[d][t]  = sum_s V[s][d] P^T[s][t]             (M=128, N=64, K=64)
-//         Ox^T[d][t]  = sum_i S^T[d][i] Q[t][i]             (M=128, N=64, K=dk)
-//         S^T[d][i]  += sum_s V[s][d] K'[s][i]              (M=128, N=dk, K=64)
-//   epi2  O[t][d]     = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t]
-//         S^T (fp32, TMEM) -> bf16 smem operand for the next chunk, then S^T *= gamma^L_next
+//         Ox^T[d][t]  = sum_i S^T[d][i] Q[t][i]             (A = bf16 S^T in TMEM)
+//         S^T[d][i]  <- gamma^L S^T + sum_s gamma^(L-1-s) V[s][d] K[s][i]
+//   out   O[t][d]     = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t]
 //
-// Warp roles (320 threads): warps 0-3 epilogue-1 (P^T mask on lanes 0-63, K' scaling),
-// warps 4-7 epilogue-2 (outputs and state), warp 8 TMA producer, warp 9 MMA issuer
-// and TMEM owner.  Q/K/V chunks stream through an mbarrier ring of STAGES slots;
-// all operands are bf16 in 128B-swizzled shared memory; accumulators are fp32 in TMEM.
+// v2:  dk <= 128 (configs[1], configs[4]) -- running state in registers of 8 state warps.
+// v3:  dk = 256 (configs[2]) -- state in TMEM, lazy scalar decay normalisation, 4-CTA clusters
+//      sharing Q/K by TMA multicast.
+// Both take a SegArgs geometry (blockIdx.z = segment) for the sequence split.
 #include <cstdlib>
 #include <mutex>
 #include <cudaTypedefs.h>
@@ -32,340 +30,7 @@ using namespace sm100;
 
 constexpr int kC = 64;          // tokens per chunk
 constexpr int kDVT = 128;       // dv rows per CTA (MMA M)
-constexpr int kThreads = 320;
 constexpr uint32_t kTmemCols = 512;
-// TMEM column map
-constexpr uint32_t T_PT = 0, T_OI = 64, T_OX = 128, T_S = 256;
-
-template <int DK, int STAGES>
-struct Cfg {
-  static constexpr int KB = DK / 64;
-  static constexpr int Q_BYTES = kC * DK * 2;
-  static constexpr int K_BYTES = kC * DK * 2;
-  static constexpr int V_BYTES = kC * kDVT * 2;
-  static constexpr int STAGE_BYTES = Q_BYTES + K_BYTES + V_BYTES;
-  static constexpr int OFF_PT = STAGES * STAGE_BYTES;
-  static constexpr int PT_BYTES = kC * kC * 2;
-  static constexpr int OFF_ST = OFF_PT + PT_BYTES;
-  static constexpr int ST_BYTES = kDVT * DK * 2;
-  static constexpr int OFF_POW = OFF_ST + ST_BYTES;
-  static constexpr int OFF_BAR = OFF_POW + 128 * 4;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;  // barriers + TMEM slot + alignment slack
-};
-
-__device__ __forceinline__ uint4 scale_bf16x8(uint4 x, float w) {
-  uint32_t* u = reinterpret_cast<uint32_t*>(&x);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float lo = __uint_as_float(u[i] << 16) * w;
-    const float hi = __uint_as_float(u[i] & 0xFFFF0000u) * w;
-    u[i] = pack_bf16x2(lo, hi);
-  }
-  return x;
-}
-
-// Write 32 fp32 values (columns col0..col0+31 of row `row`) as bf16 into a K-major
-// SW128 operand whose 64-column blocks are `block_bytes` apart.
-__device__ __forceinline__ void store_row_bf16_sw128(uint8_t* base, int block_bytes, int row,
-                                                     int col0, const float (&v)[32]) {
-  uint8_t* blk = base + (col0 / 64) * block_bytes + row * 128;
-  const int c0 = (col0 % 64) / 8;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint4 pk;
-    pk.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
-    pk.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
-    pk.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
-    pk.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
-    *reinterpret_cast<uint4*>(blk + (((c0 + j) ^ (row & 7)) << 4)) = pk;
-  }
-}
-
-template <int DK, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
-prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                  const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
-                  const float* __restrict__ log2g, const float* __restrict__ s_in,
-                  float* __restrict__ s_out, int H, int N, int dv, int state_only,
-                  const SegArgs sa, unsigned long long* __restrict__ trace) {
-  using G = Cfg<DK, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
-  uint64_t* empty = full + STAGES;
-  uint64_t* mma1_bar = empty + STAGES;
-  uint64_t* epi1_bar = mma1_bar + 1;
-  uint64_t* mma2_bar = epi1_bar + 1;
-  uint64_t* epi2_bar = mma2_bar + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi2_bar + 1);
-  float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);  // pw[n] = gamma^n, n = 0..64
-  uint8_t* pt_smem = smem + G::OFF_PT;
-  uint8_t* st_smem = smem + G::OFF_ST;
-
-  const uint32_t warp = warp_id();
-  const uint32_t lane = threadIdx.x & 31;
-  const int bh = blockIdx.y;
-  const int j0 = blockIdx.x * kDVT;
-  int lo, hi;  // this CTA's token segment (SegArgs)
-  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
-  const int nchunks = hi > lo ? (hi - lo + kC - 1) / kC : 0;
-  const size_t per_state = (size_t)gridDim.y * DK * dv;
-  const float lg = log2g[bh % H];
-
-  if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
-  if (warp == 8 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(mma1_bar, 1);
-    mbar_init(epi1_bar, state_only ? 64 : 128);  // state pass: only the K' warps arrive
-    mbar_init(mma2_bar, 1);
-    mbar_init(epi2_bar, 128);
-    fence_barrier_init();
-    if (!state_only) tma_prefetch_desc(&tm_q);
-    tma_prefetch_desc(&tm_k);
-    tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 9) tmem_alloc<kTmemCols>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-  // optional per-chunk timestamps of CTA (0, 0) for pipeline analysis (trace[event * 4096 + chunk])
-  const bool tracing = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
-#define LA_TRACE(ev, c) \
-  do { if (tracing && (c) < 4096) trace[(ev) * 4096 + (c)] = clock64(); } while (0)
-
-  if (warp == 8) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES + G::V_BYTES;
-      for (int c = 0; c < nchunks; ++c) {
-        const int s = c % STAGES;
-        const int use = c / STAGES;
-        mbar_wait(&empty[s], (use & 1) ^ 1);
-        uint8_t* st = smem + s * G::STAGE_BYTES;
-        LA_TRACE(0, c);
-        mbar_arrive_expect_tx(&full[s], bytes);
-#pragma unroll
-        for (int kb = 0; kb < G::KB; ++kb) {
-          if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);
-          tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh);
-        }
-#pragma unroll
-        for (int nb = 0; nb < kDVT / 64; ++nb)
-          tma_load_3d(st + G::Q_BYTES + G::K_BYTES + nb * 8192, &tm_v, &full[s], j0 + nb * 64,
-                      lo + c * kC, bh);
-      }
-    }
-  } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t id_qk = idesc_bf16(128, kC, false, false);   // P^T = K Q^T
-      constexpr uint32_t id_vp = idesc_bf16(128, kC, true, true);     // Oi^T = V^T P^T
-      constexpr uint32_t id_sq = idesc_bf16(128, kC, false, false);   // Ox^T = S^T Q^T
-      constexpr uint32_t id_vk = idesc_bf16(128, DK, true, true);     // S^T += V^T K'
-      const uint32_t pt_addr = smem_u32(pt_smem);
-      const uint32_t st_addr = smem_u32(st_smem);
-      for (int c = 0; c < nchunks; ++c) {
-        const int s = c % STAGES;
-        const int use = c / STAGES;
-        mbar_wait(&full[s], use & 1);
-        LA_TRACE(1, c);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(smem + s * G::STAGE_BYTES);
-        const uint32_t k_addr = q_addr + G::Q_BYTES;
-        const uint32_t v_addr = k_addr + G::K_BYTES;
-        if (!state_only) {
-#pragma unroll
-          for (int kb = 0; kb < G::KB; ++kb)
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ss(tbase + T_PT, smem_desc_sw128(k_addr + kb * 8192 + kk * 32, 16, 1024),
-                          smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_qk,
-                          (kb | kk) != 0);
-          mma_commit(mma1_bar);
-        }
-        mbar_wait(epi1_bar, c & 1);
-        LA_TRACE(2, c);
-        mbar_wait(epi2_bar, c & 1);
-        LA_TRACE(3, c);
-        tc_fence_after();
-        if (!state_only) {
-#pragma unroll
-          for (int ks = 0; ks < kC / 16; ++ks)
-            mma_bf16_ss(tbase + T_OI, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
-                        smem_desc_sw128(pt_addr + ks * 2048, 8192, 1024), id_vp, ks != 0);
-#pragma unroll
-          for (int kb = 0; kb < G::KB; ++kb)
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ss(tbase + T_OX, smem_desc_sw128(st_addr + kb * (kDVT * 128) + kk * 32, 16, 1024),
-                          smem_desc_sw128(q_addr + kb * 8192 + kk * 32, 16, 1024), id_sq,
-                          (kb | kk) != 0);
-        }
-#pragma unroll
-        for (int ks = 0; ks < kC / 16; ++ks)
-          mma_bf16_ss(tbase + T_S, smem_desc_sw128(v_addr + ks * 2048, 8192, 1024),
-                      smem_desc_sw128(k_addr + ks * 2048, 8192, 1024), id_vk, 1);
-        mma_commit(mma2_bar);
-        mma_commit(&empty[s]);
-      }
-    }
-  } else if (warp < 4) {
-    // ------------------------------------------------------------ epilogue 1
-    // (in the state pass the P^T warps have no work and must not arrive: an mbarrier
-    //  cannot tell arrivals of different chunks apart, so idle warps would lap)
-    for (int c = 0; c < (state_only && warp < 2 ? 0 : nchunks); ++c) {
-      const int s = c % STAGES;
-      const int use = c / STAGES;
-      const int L = min(kC, hi - lo - c * kC);
-      mbar_wait(&full[s], use & 1);
-      // MMA1 reads K unscaled: both the P^T warps and the K' warps wait for it
-      if (!state_only) {
-        mbar_wait(mma1_bar, c & 1);
-        tc_fence_after();
-      }
-      if (threadIdx.x == 0) LA_TRACE(4, c);
-      uint8_t* k_smem = smem + s * G::STAGE_BYTES + G::Q_BYTES;
-      if (warp < 2) {
-        if (!state_only) {
-          const int srow = warp * 32 + lane;
-          const uint32_t ta = tbase + ((warp * 32) << 16) + T_PT;
-          float p0[32], p1[32];
-          tmem_ld32(ta, p0);
-          tmem_ld32(ta + 32, p1);
-          tmem_wait_ld();
-          uint8_t* row = pt_smem + srow * 128;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float m[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int t = 8 * j + e;
-              const float pv = t < 32 ? p0[t] : p1[t - 32];
-              m[e] = t >= srow ? pv * pw[(t - srow) & 63] : 0.f;
-            }
-            uint4 pk;
-            pk.x = pack_bf16x2(m[0], m[1]);
-            pk.y = pack_bf16x2(m[2], m[3]);
-            pk.z = pack_bf16x2(m[4], m[5]);
-            pk.w = pack_bf16x2(m[6], m[7]);
-            *reinterpret_cast<uint4*>(row + ((j ^ (srow & 7)) << 4)) = pk;
-          }
-        }
-      } else {
-        const int srow = (warp - 2) * 32 + lane;
-        const float w = srow < L ? pw[L - 1 - srow] : 0.f;
-#pragma unroll
-        for (int kb = 0; kb < G::KB; ++kb) {
-          uint8_t* row = k_smem + kb * 8192 + srow * 128;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint4* p = reinterpret_cast<uint4*>(row + ((j ^ (srow & 7)) << 4));
-            *p = scale_bf16x8(*p, w);
-          }
-        }
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      if (threadIdx.x == 0 || threadIdx.x == 64) LA_TRACE(threadIdx.x == 0 ? 5 : 6, c);
-      mbar_arrive(epi1_bar);
-    }
-  } else {
-    // ------------------------------------------------------------ epilogue 2
-    const int sub = warp - 4;                 // TMEM subpartition of this warp
-    const int d = sub * 32 + lane;            // dv row within the tile
-    const int jd = j0 + d;
-    const bool dv_ok = jd < dv;
-    const uint32_t ta = tbase + ((sub * 32) << 16);
-    {
-      const float carry = pw[max(0, min(kC, hi - lo))];
-      const float w_in = gpow(lg, (float)lo);
-      for (int cb = 0; cb < DK / 32; ++cb) {
-        float sv[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          sv[i] = (s_in && dv_ok) ? w_in * s_in[((size_t)bh * DK + cb * 32 + i) * dv + jd] : 0.f;
-        for (int qi = 0; qi < sa.nloc; ++qi) {
-          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
-          if (wq < 0.f || !dv_ok) continue;
-          const float* lq = sa.loc + qi * per_state + ((size_t)bh * DK + cb * 32) * dv + jd;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) sv[i] = fmaf(wq, lq[(size_t)i * dv], sv[i]);
-        }
-        if (nchunks == 0 && s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1)) {
-          float* so = s_out + (state_only ? blockIdx.z * per_state : 0);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) so[((size_t)bh * DK + cb * 32 + i) * dv + jd] = sv[i];
-        }
-        store_row_bf16_sw128(st_smem, kDVT * 128, d, cb * 32, sv);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) sv[i] *= carry;
-        tmem_st32(ta + T_S + cb * 32, sv);
-      }
-      tmem_wait_st();
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(epi2_bar);
-    }
-    for (int c = 0; c < nchunks; ++c) {
-      const int L = min(kC, hi - lo - c * kC);
-      const bool last = c == nchunks - 1;
-      mbar_wait(mma2_bar, c & 1);
-      if (threadIdx.x == 128) LA_TRACE(7, c);
-      tc_fence_after();
-      if (!state_only) {
-        __nv_bfloat16* orow = o + ((size_t)bh * N + (size_t)lo + (size_t)c * kC) * dv + jd;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float a[32], b[32];
-          tmem_ld32(ta + T_OI + half * 32, a);
-          tmem_ld32(ta + T_OX + half * 32, b);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int t = half * 32 + i;
-            if (t < L && dv_ok) orow[(size_t)t * dv] = __float2bfloat16_rn(fmaf(pw[t + 1], b[i], a[i]));
-          }
-        }
-      }
-      const float carry = last ? 0.f : pw[min(kC, N - (c + 1) * kC)];
-      for (int cb = 0; cb < DK / 32; ++cb) {
-        float sv[32];
-        tmem_ld32(ta + T_S + cb * 32, sv);
-        tmem_wait_ld();
-        if (last) {
-          if (s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1)) {
-            float* so = s_out + (state_only ? blockIdx.z * per_state : 0);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) so[((size_t)bh * DK + cb * 32 + i) * dv + jd] = sv[i];
-          }
-        } else {
-          store_row_bf16_sw128(st_smem, kDVT * 128, d, cb * 32, sv);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) sv[i] *= carry;
-          tmem_st32(ta + T_S + cb * 32, sv);
-        }
-      }
-      if (threadIdx.x == 128) LA_TRACE(8, c);
-      if (!last) {
-        tmem_wait_st();
-        fence_proxy_async_smem();
-        tc_fence_before();
-        if (threadIdx.x == 128) LA_TRACE(9, c);
-        mbar_arrive(epi2_bar);
-      }
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 9) tmem_dealloc<kTmemCols>(tbase);
-}
-
 // ============================================================================================
 // Pipelined variant for dk <= 128 (the configs[1] hot path).  Same algebra, organised so the
 // per-chunk serial chain is short and every epilogue is a few instructions per element:
@@ -1385,31 +1050,6 @@ bool make_map(CUtensorMap* map, const void* base, int64_t D, int64_t N, int64_t 
                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
-}
-
-template <int DK, int STAGES>
-cudaError_t launch_dk(const void* q, const void* k, const void* v, void* o, const float* log2g,
-                      const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
-                      const SegArgs& sa, int nz, cudaStream_t stream) {
-  using G = Cfg<DK, STAGES>;
-  static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
-  CUtensorMap mq, mk, mv;
-  const int64_t BH = s.B * s.H;
-  if (!make_map(&mk, k, s.dk, s.N, BH) || !make_map(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
-  if (state_only) {
-    mq = mk;
-  } else if (!make_map(&mq, q, s.dk, s.N, BH)) {
-    return cudaErrorInvalidValue;
-  }
-  auto kern = prefill_tc_kernel<DK, STAGES>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-  if (err != cudaSuccess) return err;
-  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
-  kern<<<grid, kThreads, G::SMEM, stream>>>(mq, mk, mv, (__nv_bfloat16*)o, log2g, s_in, s_out,
-                                            (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
-                                            sa, g_trace);
-  count_launch();
-  return cudaGetLastError();
 }
 
 template <int DK, int STAGES>
