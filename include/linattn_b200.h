@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define LINATTN_ABI_VERSION 1
+#define LINATTN_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define LINATTN_API __attribute__((visibility("default")))
@@ -118,16 +118,28 @@ LINATTN_API int linattn_state_pass_segmented(const void* k, const void* v, float
                                              int64_t dk, int64_t dv, int dtype, int kernel,
                                              int64_t seg_len, int64_t m, int64_t nseg, void* stream);
 
+/* Inclusive prefixes: incl[p] = state at token min(N, (p+1)*seg_len), p < nseg, accumulated from a
+ * zero state over the local states of linattn_state_pass_segmented (geometry loc_seg_len, loc_m;
+ * seg_len a multiple of loc_seg_len).  incl: [nseg][B][H][dk][dv] fp32.  With nseg = ceil(N/seg_len)
+ * the last entry is the end state of the whole sequence (the per-rank state that sequence
+ * parallelism all-gathers). */
+LINATTN_API int linattn_segment_prefix(const float* loc, int64_t loc_seg_len, int64_t loc_m, int64_t nloc,
+                                       float* incl, int64_t seg_len, int64_t nseg, const float* log2g,
+                                       int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv,
+                                       void* stream);
+
 /* Prefill with every segment of seg_len tokens running in parallel, each seeded from s_in
- * (nullable; the state before token 0) and the nloc local states `loc` produced by
- * linattn_state_pass_segmented with geometry (loc_seg_len, loc_m).  The caller guarantees loc
- * covers every token before the last segment.  s_out (nullable) receives the end state. */
+ * (nullable; the state before token 0) and the nloc states `loc`: either local states produced by
+ * linattn_state_pass_segmented with geometry (loc_seg_len, loc_m) (loc_inclusive = 0), or
+ * inclusive prefixes from linattn_segment_prefix (loc_inclusive = 1, loc_m = 1, each segment
+ * reads only the entry ending at its first token).  The caller guarantees loc covers every token
+ * before the last segment.  s_out (nullable) receives the end state. */
 LINATTN_API int linattn_prefill_segmented(const void* q, const void* k, const void* v, void* o,
                                           const float* log2g, const float* s_in, float* s_out,
                                           const float* loc, int64_t loc_seg_len, int64_t loc_m,
-                                          int64_t nloc, int64_t B, int64_t H, int64_t N, int64_t dk,
-                                          int64_t dv, int dtype, int kernel, int64_t seg_len,
-                                          void* stream);
+                                          int64_t nloc, int loc_inclusive, int64_t B, int64_t H,
+                                          int64_t N, int64_t dk, int64_t dv, int dtype, int kernel,
+                                          int64_t seg_len, void* stream);
 
 /* out = gamma^pos * s_in + sum_{z: hi_z <= pos} gamma^(pos - hi_z) * loc[z]   ([B,H,dk,dv] fp32);
  * with pos == N this is the end state of the whole sequence from its segment-local states. */

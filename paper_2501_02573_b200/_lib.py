@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("LINATTN_LIB") or os.path.join(
 OK, ESHAPE, EPARAM, EDTYPE, EUNSUPPORTED, ECUDA = range(6)
 F32, BF16 = 0, 1
 KERNEL_AUTO, KERNEL_TC, KERNEL_SIMT = 0, 1, 2
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
 
@@ -35,8 +35,9 @@ _SIGS = {
     "linattn_seq_plan": [_i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i64)],
     "linattn_state_pass_segmented": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int,
                                      ctypes.c_int, _i64, _i64, _i64, _vp],
-    "linattn_prefill_segmented": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64,
-                                  _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _i64, _vp],
+    "linattn_prefill_segmented": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_int,
+                                  _i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _i64, _vp],
+    "linattn_segment_prefix": [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
     "linattn_state_at": [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
     "linattn_last_error": [],
     "linattn_abi_version": [],

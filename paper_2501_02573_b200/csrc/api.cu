@@ -183,15 +183,25 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
   if (pl.nseg > 1) {
     // two-phase split: local states of segments 0..nseg-2 (m-way sub-split), then every
     // segment seeded from them in its prologue; workspace from the library's stream pool
+    // (the prefix scan turns the m-way local states into one inclusive state per segment end,
+    //  so each seeded CTA reads a single 64 KiB state in its prologue)
     const int64_t nloc = (pl.nseg - 1) * pl.m;
-    const size_t bytes = (size_t)nloc * s.B * s.H * s.dk * s.dv * sizeof(float);
+    const size_t per = (size_t)s.B * s.H * s.dk * s.dv;
+    const size_t bytes = (size_t)(nloc + pl.nseg - 1) * per * sizeof(float);
     float* loc = nullptr;
     cudaMemPool_t pool = work_pool();
     if (pool && cudaMallocFromPoolAsync((void**)&loc, bytes, pool, st) == cudaSuccess) {
+      float* incl = loc + (size_t)nloc * per;
       cudaError_t e = launch(nullptr, nullptr, nullptr, loc, true, make_seg(pl.seg_len, pl.m), (int)nloc);
       if (e == cudaSuccess) {
+        SegArgs a = make_seg(s.N, 1);
+        attach_loc(a, loc, pl.seg_len, pl.m, nloc);
+        e = launch_segment_prefix(a, incl, pl.seg_len, pl.nseg - 1, log2g, s, st);
+      }
+      if (e == cudaSuccess) {
         SegArgs b = make_seg(pl.seg_len, 1);
-        attach_loc(b, loc, pl.seg_len, pl.m, nloc);
+        attach_loc(b, incl, pl.seg_len, 1, pl.nseg - 1);
+        b.loc_incl = 1;
         e = launch(q, o, s_in, s_out, false, b, (int)pl.nseg);
       }
       cudaFreeAsync(loc, st);
@@ -269,8 +279,9 @@ int linattn_state_pass_segmented(const void* k, const void* v, float* loc_out, c
 
 int linattn_prefill_segmented(const void* q, const void* k, const void* v, void* o, const float* log2g,
                               const float* s_in, float* s_out, const float* loc, int64_t loc_seg_len,
-                              int64_t loc_m, int64_t nloc, int64_t B, int64_t H, int64_t N, int64_t dk,
-                              int64_t dv, int dtype, int kernel, int64_t seg_len, void* stream) {
+                              int64_t loc_m, int64_t nloc, int loc_inclusive, int64_t B, int64_t H,
+                              int64_t N, int64_t dk, int64_t dv, int dtype, int kernel, int64_t seg_len,
+                              void* stream) {
   ShapeArgs s{B, H, N, dk, dv};
   if (int e = check_dims(s, true)) return e;
   if (int e = check_dtype(dtype)) return e;
@@ -284,14 +295,34 @@ int linattn_prefill_segmented(const void* q, const void* k, const void* v, void*
                 (long long)loc_seg_len, (long long)loc_m, (long long)nloc);
   const int64_t nseg = ceil_div(N, seg_len);
   if (nseg > 65535) return fail(LINATTN_EPARAM, "too many segments (%lld)", (long long)nseg);
+  if (loc && loc_inclusive && (seg_len % loc_seg_len != 0 || loc_m != 1))
+    return fail(LINATTN_EPARAM, "inclusive states need loc_m == 1 and segments aligned to their ends");
   SegArgs a = make_seg(seg_len, 1);
   attach_loc(a, loc, loc_seg_len, loc_m, nloc);
+  a.loc_incl = loc_inclusive ? 1 : 0;
   cudaStream_t st = (cudaStream_t)stream;
   if (tc)
     return cuda_status(launch_prefill_tc(q, k, v, o, log2g, s_in, s_out, s, false, a, (int)nseg, st),
                        "prefill_tc (segmented)");
   return cuda_status(launch_prefill_simt(q, k, v, o, log2g, s_in, s_out, s, dtype, false, a, (int)nseg, st),
                      "prefill_simt (segmented)");
+}
+
+int linattn_segment_prefix(const float* loc, int64_t loc_seg_len, int64_t loc_m, int64_t nloc, float* incl,
+                           int64_t seg_len, int64_t nseg, const float* log2g, int64_t B, int64_t H, int64_t N,
+                           int64_t dk, int64_t dv, void* stream) {
+  ShapeArgs s{B, H, N, dk, dv};
+  if (int e = check_dims(s, true)) return e;
+  if (!loc || !incl || !log2g) return fail(LINATTN_EPARAM, "null pointer");
+  if (loc_seg_len < 1 || loc_m < 1 || nloc < 1 || nloc > ceil_div(N, loc_seg_len) * loc_m)
+    return fail(LINATTN_EPARAM, "bad local-state geometry");
+  if (seg_len < 1 || nseg < 1 || nseg > ceil_div(N, seg_len) || seg_len % loc_seg_len != 0)
+    return fail(LINATTN_EPARAM, "prefix segments (%lld x %lld) must be unions of local segments of %lld",
+                (long long)nseg, (long long)seg_len, (long long)loc_seg_len);
+  SegArgs a = make_seg(N, 1);
+  attach_loc(a, loc, loc_seg_len, loc_m, nloc);
+  return cuda_status(launch_segment_prefix(a, incl, seg_len, nseg, log2g, s, (cudaStream_t)stream),
+                     "segment_prefix");
 }
 
 int linattn_state_at(const float* loc, int64_t loc_seg_len, int64_t loc_m, int64_t nloc, const float* s_in,

@@ -47,10 +47,14 @@ struct ShapeArgs {
 // at token lo is seeded with
 //     S_init = gamma^lo * s_in + sum_{q : hi_q <= lo} gamma^(lo - hi_q) * loc[q]
 // which is the reference recursion cross term (kernels.py:185-189) applied across segments.
+//
+// Inclusive mode (loc_incl = 1): loc[q] is instead the prefix state at token min(N, (q+1)*loc_seg_len)
+// from a zero state (linattn_segment_prefix), so a segment starting at lo > 0 reads the single
+// entry ending at lo with weight 1 -- one 64 KiB state per CTA instead of every earlier entry.
 struct SegArgs {
   int seg_len = 0x7fffffff, sub = 0x7fffffff, m = 1;
   const float* loc = nullptr;
-  int loc_seg_len = 0, loc_sub = 0, loc_m = 1, nloc = 0;
+  int loc_seg_len = 0, loc_sub = 0, loc_m = 1, nloc = 0, loc_incl = 0;
 };
 
 __host__ __device__ __forceinline__ void seg_bounds(int seg_len, int sub, int m, int z, int N, int& lo,
@@ -66,6 +70,10 @@ __host__ __device__ __forceinline__ void seg_bounds(int seg_len, int sub, int m,
 // Weight of loc entry q for a segment starting at `lo`: gamma^(lo - hi_q) if the entry lies
 // entirely before lo, else 0 (returned as a negative flag).
 __device__ __forceinline__ float seg_loc_weight(const SegArgs& sa, int q, int N, int lo, float lg) {
+  if (sa.loc_incl) {
+    const long long end = min((long long)(q + 1) * sa.loc_seg_len, (long long)N);
+    return (lo > 0 && end == lo) ? 1.f : -1.f;
+  }
   int qlo, qhi;
   seg_bounds(sa.loc_seg_len, sa.loc_sub, sa.loc_m, q, N, qlo, qhi);
   if (qhi > lo || qhi <= qlo) return -1.f;
@@ -84,6 +92,11 @@ cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void*
                               const float* log2g, const float* s_in, float* s_out,
                               const ShapeArgs& s, bool state_only, const SegArgs& sa, int nz,
                               cudaStream_t stream);
+
+// Inclusive prefixes incl[p] = state at min(N, (p+1)*seg_len) for p < nseg, from the local states
+// `sa.loc` of a state-only launch (geometry in sa.loc_*): one running scan per element.
+cudaError_t launch_segment_prefix(const SegArgs& sa, float* incl, int64_t seg_len, int64_t nseg,
+                                  const float* log2g, const ShapeArgs& s, cudaStream_t stream);
 
 // State at token position `pos` from segment-local states (elementwise over [B*H][dk][dv]):
 //   out = gamma^pos * s_in + sum_{q : hi_q <= pos} gamma^(pos - hi_q) * loc[q]

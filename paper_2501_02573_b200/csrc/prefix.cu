@@ -3,6 +3,8 @@
 // evaluated as the scan acc <- gamma^(L_q) acc + S_q over q = 0 .. rank-1 (the
 // recursion cross-term weights of the reference, kernels.py:185-189, applied
 // across sequence segments).  Elementwise over [B, H, dk, dv]; float4 accesses.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace linattn {
@@ -70,7 +72,50 @@ __global__ void state_at_kernel(const float4* __restrict__ loc, const float4* __
   out[idx] = acc;
 }
 
+// incl[p] = state at H_p = min(N, (p+1)*seg_len) accumulated from the ordered local states:
+// acc (state at `pos`) <- gamma^(hi_q - pos) acc + loc[q] for each entry q, emitted at each H_p.
+__global__ void segment_prefix_kernel(const float4* __restrict__ loc, float4* __restrict__ incl,
+                                      const SegArgs sa, int N, int seg_len, int nseg,
+                                      const float* __restrict__ log2g, int H, int64_t per_head4,
+                                      int64_t per_state4) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= per_state4) return;
+  const float lg = log2g[(int)((idx / per_head4) % H)];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int pos = 0, q = 0;
+  for (int p = 0; p < nseg; ++p) {
+    const int hp = (int)min((long long)(p + 1) * seg_len, (long long)N);
+    for (; q < sa.nloc; ++q) {
+      int qlo, qhi;
+      seg_bounds(sa.loc_seg_len, sa.loc_sub, sa.loc_m, q, N, qlo, qhi);
+      if (qhi > hp) break;
+      if (qhi <= qlo) continue;                         // empty sub-segment
+      const float w = gpow(lg, (float)(qhi - pos));
+      const float4 x = loc[(int64_t)q * per_state4 + idx];
+      acc = make_float4(fmaf(w, acc.x, x.x), fmaf(w, acc.y, x.y), fmaf(w, acc.z, x.z), fmaf(w, acc.w, x.w));
+      pos = qhi;
+    }
+    const float w = gpow(lg, (float)(hp - pos));
+    incl[(int64_t)p * per_state4 + idx] = make_float4(w * acc.x, w * acc.y, w * acc.z, w * acc.w);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_segment_prefix(const SegArgs& sa, float* incl, int64_t seg_len, int64_t nseg,
+                                  const float* log2g, const ShapeArgs& s, cudaStream_t stream) {
+  const int64_t per_head = s.dk * s.dv;
+  if (per_head % 4 != 0) return cudaErrorNotSupported;
+  for (const void* p : {(const void*)sa.loc, (const void*)incl})
+    if (reinterpret_cast<uintptr_t>(p) & 15) return cudaErrorNotSupported;
+  const int64_t n4 = s.B * s.H * per_head / 4;
+  constexpr int NT = 256;
+  segment_prefix_kernel<<<(unsigned)((n4 + NT - 1) / NT), NT, 0, stream>>>(
+      (const float4*)sa.loc, (float4*)incl, sa, (int)s.N, (int)std::min<int64_t>(seg_len, 0x7fffffff),
+      (int)nseg, log2g, (int)s.H, per_head / 4, n4);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_state_at(const float* loc, const float* s_in, float* out, const SegArgs& sa,
                             int64_t pos, const float* log2g, const ShapeArgs& s, cudaStream_t stream) {

@@ -82,9 +82,12 @@ def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "a
         seg = -(-n // seq_split)
         seg = -(-seg // 64) * 64 if seg < n else n
         nseg = -(-n // seg)
-        loc = state_pass_segmented(k, v, log2g, seg, m=1, nseg=nseg - 1, kernel=kernel) if nseg > 1 else None
-        return prefill_segmented(q, k, v, log2g, seg, loc=loc, loc_geom=(seg, 1), s_in=s_in, s_out=s_out,
-                                 out=out, kernel=kernel)
+        incl = None
+        if nseg > 1:
+            loc = state_pass_segmented(k, v, log2g, seg, m=1, nseg=nseg - 1, kernel=kernel)
+            incl = segment_prefix(loc, (seg, 1), seg, nseg - 1, log2g, n)
+        return prefill_segmented(q, k, v, log2g, seg, loc=incl, loc_geom=(seg, 1), inclusive=True, s_in=s_in,
+                                 s_out=s_out, out=out, kernel=kernel)
     if seq_split == 1:
         return prefill_segmented(q, k, v, log2g, q.shape[2], s_in=s_in, s_out=s_out, out=out, kernel=kernel)
     _require_cuda(q, k, v, log2g, s_in, s_out, out)
@@ -148,10 +151,24 @@ def state_pass_segmented(k, v, log2g, seg_len: int, *, m: int = 1, nseg: int | N
     return out
 
 
-def prefill_segmented(q, k, v, log2g, seg_len: int, *, loc=None, loc_geom=None, s_in=None, s_out=None,
-                      out=None, kernel: str = "auto"):
-    """Prefill with every seg_len-token segment in parallel, seeded from s_in and the local
-    states ``loc`` (from ``state_pass_segmented`` with geometry ``loc_geom = (seg_len, m)``)."""
+def segment_prefix(loc, loc_geom, seg_len: int, nseg: int, log2g, n: int, *, out=None):
+    """Inclusive prefix states incl[p] at token min(n, (p+1)*seg_len), p < nseg, from the local
+    states ``loc`` of ``state_pass_segmented`` (geometry ``loc_geom``); [nseg, B, H, dk, dv]."""
+    _require_cuda(loc, log2g, out)
+    _, B, H, dk, dv = loc.shape
+    if out is None:
+        out = torch.empty((nseg, B, H, dk, dv), dtype=torch.float32, device=loc.device)
+    lib = _lib.load()
+    _lib.check(lib.linattn_segment_prefix(loc.data_ptr(), loc_geom[0], loc_geom[1], loc.shape[0], out.data_ptr(),
+                                          seg_len, nseg, log2g.data_ptr(), B, H, n, dk, dv, _stream()))
+    return out
+
+
+def prefill_segmented(q, k, v, log2g, seg_len: int, *, loc=None, loc_geom=None, inclusive: bool = False,
+                      s_in=None, s_out=None, out=None, kernel: str = "auto"):
+    """Prefill with every seg_len-token segment in parallel, seeded from s_in and ``loc``: local
+    states from ``state_pass_segmented`` (geometry ``loc_geom = (seg_len, m)``), or, with
+    ``inclusive``, prefix states from ``segment_prefix`` (one read per segment)."""
     _require_cuda(q, k, v, log2g, s_in, s_out, out, loc)
     B, H, N, dk = q.shape
     dv = v.shape[3]
@@ -165,8 +182,8 @@ def prefill_segmented(q, k, v, log2g, seg_len: int, *, loc=None, loc_geom=None, 
     lib = _lib.load()
     _lib.check(lib.linattn_prefill_segmented(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                              log2g.data_ptr(), _ptr(s_in), _ptr(s_out), _ptr(loc), lseg, lm,
-                                             nloc, B, H, N, dk, dv, _dtype_code(q), _KERNELS[kernel],
-                                             seg_len, _stream()))
+                                             nloc, 1 if inclusive else 0, B, H, N, dk, dv, _dtype_code(q),
+                                             _KERNELS[kernel], seg_len, _stream()))
     return out
 
 

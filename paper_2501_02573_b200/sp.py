@@ -39,31 +39,38 @@ class CudaBackend:
     """Product backend: the sm_100a kernels of liblinattn_b200.so.
 
     The local scan of a rank's segment is itself split across the SMs when batch x head
-    leaves them idle (the same two-phase algebra inside the device, ``ops.seq_plan``).
+    leaves them idle (the same two-phase algebra inside the device, ``ops.seq_plan``): one
+    state-only launch over every sub-segment, one prefix scan giving the state at each segment
+    end (the last one is the rank's end state), one seeded launch over all segments.
     """
 
     def __init__(self, kernel: str = "auto"):
         self.kernel = kernel
 
     def local_states(self, k, v, log2g):
-        """Segment-local end states of this rank's tokens and their geometry (seg_len, m)."""
+        """(opaque local data, this rank's end state [B, H, dk, dv] from a zero state)."""
         B, H, L, dk = k.shape
         dv = v.shape[3]
         seg, nseg, m, _ = ops.seq_plan(B, H, L, dk, dv, k.dtype, self.kernel)
         if nseg == 1:
             seg, m = L, 1
+        else:
+            # the state pass covers all nseg segments here: one wave of long CTAs beats more,
+            # shorter ones once the units already fill most SMs
+            sms = torch.cuda.get_device_properties(k.device).multi_processor_count
+            if B * H * -(-dv // 128) * nseg >= 0.8 * sms:
+                m = 1
         loc = ops.state_pass_segmented(k, v, log2g, seg, m=m, nseg=nseg, kernel=self.kernel)
-        return loc, (seg, m)
-
-    def state_at(self, loc, geom, pos, log2g):
-        return ops.state_at(loc, geom, pos, log2g, pos)
+        incl = ops.segment_prefix(loc, (seg, m), seg, nseg, log2g, L)
+        return (incl, seg), incl[-1]
 
     def prefix_combine(self, gathered, seg_lens, rank, log2g):
         return ops.prefix_combine(gathered, seg_lens, rank, log2g)
 
-    def prefill(self, q, k, v, log2g, s_in, loc, geom):
-        return ops.prefill_segmented(q, k, v, log2g, geom[0], loc=loc, loc_geom=geom, s_in=s_in,
-                                     kernel=self.kernel)
+    def prefill(self, q, k, v, log2g, s_in, local):
+        incl, seg = local
+        return ops.prefill_segmented(q, k, v, log2g, seg, loc=incl[:-1] if incl.shape[0] > 1 else None,
+                                     loc_geom=(seg, 1), inclusive=True, s_in=s_in, kernel=self.kernel)
 
 
 def sp_prefill(q_seg, k_seg, v_seg, log2g, seg_lens, group=None, backend=None):
@@ -83,8 +90,7 @@ def sp_prefill(q_seg, k_seg, v_seg, log2g, seg_lens, group=None, backend=None):
         raise ValueError(f"seg_lens has {len(seg_lens)} entries for world size {world}")
     if k_seg.shape[2] != seg_lens[rank]:
         raise ValueError(f"rank {rank} holds {k_seg.shape[2]} tokens, seg_lens says {seg_lens[rank]}")
-    loc, geom = backend.local_states(k_seg, v_seg, log2g)         # segment-local, zero state
-    local = backend.state_at(loc, geom, k_seg.shape[2], log2g)     # this rank's end state [B,H,dk,dv]
+    local_data, local = backend.local_states(k_seg, v_seg, log2g)   # end state from zero [B,H,dk,dv]
     if world > 1:
         local = local.contiguous()
         # gloo has no device all-gather: stage through the host (CPU tests, shared-GPU path checks)
@@ -97,4 +103,4 @@ def sp_prefill(q_seg, k_seg, v_seg, log2g, seg_lens, group=None, backend=None):
     else:
         gathered = local[None]
     s_in = backend.prefix_combine(gathered, seg_lens, rank, log2g) if rank > 0 else None
-    return backend.prefill(q_seg, k_seg, v_seg, log2g, s_in, loc, geom)
+    return backend.prefill(q_seg, k_seg, v_seg, log2g, s_in, local_data)

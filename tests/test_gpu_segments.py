@@ -85,6 +85,16 @@ def test_segmented_geometries(ops, seg_len, m, mode):
     # the state at N from the local states equals the seeded end state
     end = ops.state_at(loc, (seg_len, m), N, l2, N, s_in=dev(s0))
     assert orc.max_rel_error(end.cpu().numpy(), ref_s) <= (5e-3 if mode == "tc" else 1e-5)
+    # inclusive prefixes at every segment end, then the one-read-per-segment seeded prefill
+    incl = ops.segment_prefix(loc, (seg_len, m), seg_len, nseg, l2, N)
+    for p in (0, nseg // 2, nseg - 1):
+        hi = min(N, (p + 1) * seg_len)
+        want = np.stack([[orc.segment_end_state(c[x, h, :hi], v[x, h, :hi], gam[h]) for h in range(H)]
+                         for x in range(B)])
+        assert orc.max_rel_error(incl[p].cpu().numpy(), want) <= (5e-3 if mode == "tc" else 1e-5)
+    out2 = ops.prefill_segmented(q, k, vv, l2, seg_len, loc=incl[:-1] if nseg > 1 else None, loc_geom=(seg_len, 1),
+                                 inclusive=True, s_in=dev(s0), kernel=kernel)
+    assert orc.max_rel_error(out2.float().cpu().numpy(), ref) <= tol
 
 
 @pytest.mark.parametrize("parts", [2, 3, 8])
@@ -98,12 +108,12 @@ def test_sp_pieces_loopback(ops, parts):
     bounds = segment_bounds(3000, parts)
     lens = [hi - lo for lo, hi in bounds]
     segs = [[dev(x[:, :, lo:hi], torch.bfloat16) for x in (b, c, v)] for lo, hi in bounds]
-    locs = [be.local_states(k, vv, l2) for _, k, vv in segs]
-    ends = torch.stack([be.state_at(loc, geom, k.shape[2], l2) for (loc, geom), (_, k, _) in zip(locs, segs)])
+    locals_ = [be.local_states(k, vv, l2) for _, k, vv in segs]
+    ends = torch.stack([end for _, end in locals_])
     outs = []
-    for r, ((q, k, vv), (loc, geom)) in enumerate(zip(segs, locs)):
+    for r, ((q, k, vv), (data, _)) in enumerate(zip(segs, locals_)):
         s_in = be.prefix_combine(ends, lens, r, l2) if r > 0 else None
-        outs.append(be.prefill(q, k, vv, l2, s_in, loc, geom))
+        outs.append(be.prefill(q, k, vv, l2, s_in, data))
     got = torch.cat(outs, dim=2).float().cpu().numpy()
     assert orc.max_rel_error(got, ref) <= TOL_BF16
 

@@ -24,11 +24,7 @@ class OracleBackend:
     def local_states(self, k, v, log2g):
         s = np.stack([[orc.segment_end_state(k[x, h].numpy(), v[x, h].numpy(), self.gammas[h], self.decay)
                        for h in range(k.shape[1])] for x in range(k.shape[0])])
-        return torch.from_numpy(s)[None], (k.shape[2], 1)
-
-    def state_at(self, loc, geom, pos, log2g):
-        assert geom == (pos, 1) and loc.shape[0] == 1   # one local segment covering the rank
-        return loc[0]
+        return None, torch.from_numpy(s)
 
     def prefix_combine(self, gathered, seg_lens, rank, log2g):
         g = gathered.numpy()
@@ -38,7 +34,7 @@ class OracleBackend:
                                                     self.gammas[h], self.decay)[rank]
         return torch.from_numpy(out)
 
-    def prefill(self, q, k, v, log2g, s_in, loc, geom):
+    def prefill(self, q, k, v, log2g, s_in, local):
         out, _ = orc.seeded_blocked_attn(q.numpy(), k.numpy(), v.numpy(), self.gammas, self.decay,
                                          None if s_in is None else s_in.numpy(), block=16)
         return torch.from_numpy(out)

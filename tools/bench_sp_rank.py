@@ -15,10 +15,9 @@ gathered = torch.zeros(8, B, H, d, d, device="cuda")
 
 
 def rank_path():
-    loc, geom = be.local_states(k, v, l2)
-    be.state_at(loc, geom, N, l2)
+    data, end = be.local_states(k, v, l2)
     si = be.prefix_combine(gathered, [N] * 8, 7, l2)
-    be.prefill(q, k, v, l2, si, loc, geom)
+    be.prefill(q, k, v, l2, si, data)
 
 
 def timeit(f, it=50):
@@ -34,3 +33,18 @@ def timeit(f, it=50):
 print(json.dumps({"plain_split_us": timeit(lambda: ops.prefill(q, k, v, l2)),
                   "sp_rank_path_us": timeit(rank_path),
                   "plan": ops.seq_plan(B, H, N, d, d)}))
+
+# the same rank path replayed from a CUDA graph (no host gaps between the five launches)
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+g = torch.cuda.CUDAGraph()
+with torch.cuda.stream(s):
+    rank_path()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        rank_path()
+torch.cuda.current_stream().wait_stream(s)
+print(json.dumps({"sp_rank_path_graph_us": timeit(g.replay)}))
+data, end = be.local_states(k, v, l2)
+print(json.dumps({"phaseA_and_prefix_us": timeit(lambda: be.local_states(k, v, l2)),
+                  "phaseB_us": timeit(lambda: be.prefill(q, k, v, l2, s_in, data))}))
