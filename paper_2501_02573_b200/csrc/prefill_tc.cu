@@ -138,7 +138,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
-      mbar_init(&epi1_bar[i], state_only ? 64 : 128);
+      mbar_init(&epi1_bar[i], 128);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&mma1_bar[b], 1);
@@ -181,7 +181,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
   if (warp < 4) {
     // ------------------------------------------------------------ P^T mask / K' scaling
-    for (int c = 0; c < (state_only && warp < 2 ? 0 : nchunks); ++c) {
+    for (int c = 0; c < nchunks; ++c) {
       const int s = c % STAGES;
       const int b = c & 1;
       const int L = min(kC, hi - lo - c * kC);
@@ -190,7 +190,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         mbar_wait(mma1_bar, c & 1);                 // MMA1 has consumed the unscaled K
         tc_fence_after();
       }
-      if (warp < 2) {
+      if (warp < 2 && !state_only) {
         // P^T[s][t] *= gamma^(t-s) (t >= s), bf16: row s of the MN-major B operand of Oi
         const int srow = warp * 32 + lane;
         const uint32_t ta = tbase + ((warp * 32) << 16) + T_P;
@@ -211,7 +211,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
             *reinterpret_cast<uint4*>(row + (((half * 4 + j) ^ (srow & 7)) << 4)) = pk;
           }
         }
-      } else {
+      } else if (!state_only) {
         // K'[s] = gamma^(L-1-s) K[s], zero beyond the ragged end (in place, bf16x2 multiplies)
         const int srow = (warp - 2) * 32 + lane;
         const uint32_t w2 = pw2[srow < L ? L - 1 - srow : -64];     // pw2[-64] = (0, 0)
@@ -234,6 +234,28 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
             y.w = hmul2_bf16(y.w, wk);
             *reinterpret_cast<uint4*>(k_smem + kb * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4)) = y;
           }
+      }
+      if (state_only) {
+        // state pass: no P^T, so all four warps share K' (thread -> row, 64-column block)
+        const int tid = (int)warp * 32 + (int)lane;
+        const int srow = tid & 63;
+        const uint32_t w2 = pw2[srow < L ? L - 1 - srow : -64];
+        const uint32_t wk = (w2 & 0xFFFFu) | (w2 << 16);
+        uint8_t* k_smem = smem + s * G::STAGE_BYTES + G::Q_BYTES;
+        for (int kb = tid >> 6; kb < G::KB; kb += 2) {
+          uint4 x[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            x[j] = *reinterpret_cast<const uint4*>(k_smem + kb * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            x[j].x = hmul2_bf16(x[j].x, wk);
+            x[j].y = hmul2_bf16(x[j].y, wk);
+            x[j].z = hmul2_bf16(x[j].z, wk);
+            x[j].w = hmul2_bf16(x[j].w, wk);
+            *reinterpret_cast<uint4*>(k_smem + kb * 8192 + srow * 128 + ((j ^ (srow & 7)) << 4)) = x[j];
+          }
+        }
       }
       fence_proxy_async_smem();
       tc_fence_before();
