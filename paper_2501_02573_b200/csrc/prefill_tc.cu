@@ -63,10 +63,12 @@ constexpr int kL2Ahead = LA_L2_AHEAD;   // chunks of L2 prefetch beyond the smem
 // in shared memory (a 32 KiB read-modify-write per chunk on the mask warps' path).
 constexpr uint32_t T_P = 0, T_OX = 64, T_O = 128, T_DS = 256, T_ST = 384;
 
-template <int DK, int STAGES>
+// SO = state-only instantiation: no Q slot in the ring, so the same shared memory holds more
+// K/V stages (the state pass is bound by how many bytes each SM keeps in flight).
+template <int DK, int STAGES, bool SO = false>
 struct Cfg {
   static constexpr int KB = DK / 64;
-  static constexpr int Q_BYTES = kC * DK * 2;
+  static constexpr int Q_BYTES = SO ? 0 : kC * DK * 2;
   static constexpr int K_BYTES = kC * DK * 2;
   static constexpr int V_BYTES = kC * kDVT * 2;
   static constexpr int STAGE_BYTES = Q_BYTES + K_BYTES + V_BYTES;
@@ -88,14 +90,14 @@ __device__ __forceinline__ uint32_t hmul2_bf16(uint32_t a, uint32_t b) {
   return r;
 }
 
-template <int DK, int STAGES>
+template <int DK, int STAGES, bool SO>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                        const float* __restrict__ log2g, const float* __restrict__ s_in,
                        float* __restrict__ s_out, int H, int N, int dv, int state_only,
                        const SegArgs sa, unsigned long long* __restrict__ trace) {
-  using G = Cfg<DK, STAGES>;
+  using G = Cfg<DK, STAGES, SO>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
@@ -1074,11 +1076,11 @@ bool make_map(CUtensorMap* map, const void* base, int64_t D, int64_t N, int64_t 
   return r == CUDA_SUCCESS;
 }
 
-template <int DK, int STAGES>
+template <int DK, int STAGES, bool SO = false>
 cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, const float* log2g,
                         const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
                         const SegArgs& sa, int nz, cudaStream_t stream) {
-  using G = v2::Cfg<DK, STAGES>;
+  using G = v2::Cfg<DK, STAGES, SO>;
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
   CUtensorMap mq, mk, mv;
   const int64_t BH = s.B * s.H;
@@ -1090,7 +1092,7 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   }
   CUtensorMap mo = mk;
   if (!state_only && !make_map(&mo, o, s.dv, s.N, BH)) return cudaErrorInvalidValue;
-  auto kern = v2::prefill_tc_pipe_kernel<DK, STAGES>;
+  auto kern = v2::prefill_tc_pipe_kernel<DK, STAGES, SO>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
   dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
@@ -1176,8 +1178,12 @@ cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void*
   for (const void* p : {q, k, v, (const void*)o})
     if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return cudaErrorNotSupported;
   switch (s.dk) {
-    case 64: return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
-    case 128: return launch_pipe<128, V2_STAGES128>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
+    case 64:
+      if (state_only) return launch_pipe<64, 8, true>(q, k, v, o, log2g, s_in, s_out, s, true, sa, nz, stream);
+      return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, false, sa, nz, stream);
+    case 128:
+      if (state_only) return launch_pipe<128, 6, true>(q, k, v, o, log2g, s_in, s_out, s, true, sa, nz, stream);
+      return launch_pipe<128, V2_STAGES128>(q, k, v, o, log2g, s_in, s_out, s, false, sa, nz, stream);
     case 256: return launch_tmem_state<256, 2>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
     default: return cudaErrorNotSupported;
   }
