@@ -54,10 +54,6 @@ constexpr int kThreads = 448;
 #define V2_OT_BUFS 1
 #endif
 constexpr int kOtBufs = V2_OT_BUFS;     // output staging tiles (2: a store never blocks the next chunk)
-#ifndef LA_L2_AHEAD
-#define LA_L2_AHEAD 0
-#endif
-constexpr int kL2Ahead = LA_L2_AHEAD;   // chunks of L2 prefetch beyond the smem ring
 // TMEM column map: P^T | O_inter | O_intra x2 | dS | S^T (bf16 A operand) x2.  O_inter = S_c^T Q^T
 // is kept apart so gamma^(t+1) is applied in fp32 in the output epilogue instead of rescaling Q
 // in shared memory (a 32 KiB read-modify-write per chunk on the mask warps' path).
@@ -409,24 +405,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
           mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
           if (tracing) trace[13 * 4096 + c] = clock64();
           uint8_t* st = smem + s * G::STAGE_BYTES;
-          if (kL2Ahead > 0 && c == 0) {  // warm L2 with the first chunks too
-            for (int cp = 1; cp < STAGES + kL2Ahead && cp < nchunks; ++cp) {
-              for (int kb = 0; kb < G::KB; ++kb) {
-                if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, lo + cp * kC, bh);
-                tma_prefetch_l2_3d(&tm_k, kb * 64, lo + cp * kC, bh);
-              }
-              for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, lo + cp * kC, bh);
-            }
-          }
           mbar_arrive_expect_tx(&full[s], bytes);
-          if (kL2Ahead > 0 && c + STAGES + kL2Ahead < nchunks) {  // keep HBM requests ahead of the smem ring
-            const int cp = c + STAGES + kL2Ahead;
-            for (int kb = 0; kb < G::KB; ++kb) {
-              if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, lo + cp * kC, bh);
-              tma_prefetch_l2_3d(&tm_k, kb * 64, lo + cp * kC, bh);
-            }
-            for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 64, lo + cp * kC, bh);
-          }
 #pragma unroll
           for (int kb = 0; kb < G::KB; ++kb) {
             if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);

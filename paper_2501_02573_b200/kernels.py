@@ -154,7 +154,6 @@ def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
     compute = torch.cuda.current_stream(dev)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     s_in.wait_stream(compute)          # device buffers were allocated on the compute stream
-    done = []
     for bs, hs in _pieces(v.shape[0], v.shape[1]):
         loaded = torch.cuda.Event()
         with torch.cuda.stream(s_in):
@@ -173,7 +172,6 @@ def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
             s_out.wait_event(computed)
             src = od[bs, hs] if in_dtype == cdt else od[bs, hs].to(in_dtype)
             result[bs, hs].copy_(src, non_blocking=result.is_pinned())
-        done.append(computed)
     s_out.synchronize()
     return result
 

@@ -1,6 +1,5 @@
 """Summarise an ncu --set full report: key metrics + top stall source lines (for profiles/)."""
-import csv, io, json, subprocess, sys
-from collections import Counter
+import csv, io, subprocess, sys
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
