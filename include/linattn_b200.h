@@ -147,6 +147,14 @@ LINATTN_API int linattn_state_at(const float* loc, int64_t loc_seg_len, int64_t 
                                  const float* s_in, float* out, int64_t pos, const float* log2g,
                                  int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv, void* stream);
 
+/* The reference row-based route for a whole sequence in one launch (_row_based_slice,
+ * kernels.py:93-106): for t = 0..N-1, S <- gamma S + k_t^T v_t, o_t = q_t S, with the fp32 state
+ * in registers; s_in / s_out (nullable) seed / receive S.  Needs dk <= 256, dk and dv rows that are
+ * multiples of 16 bytes and 16-byte aligned q, k, v (tokens are staged with cp.async). */
+LINATTN_API int linattn_recurrent(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                                  const float* s_in, float* s_out, int64_t B, int64_t H, int64_t N,
+                                  int64_t dk, int64_t dv, int dtype, void* stream);
+
 /* Kernel family LINATTN_KERNEL_AUTO resolves to for this shape/dtype (TC or SIMT). */
 LINATTN_API int linattn_prefill_kernel(int64_t dk, int64_t dv, int dtype);
 

@@ -31,6 +31,7 @@ _SIGS = {
     "linattn_prefix_combine": [_vp, _vp, ctypes.POINTER(_i64), ctypes.c_int, ctypes.c_int, _vp,
                                _i64, _i64, _i64, _i64, _vp],
     "linattn_decode_step": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp],
+    "linattn_recurrent": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, _vp],
     "linattn_prefill_kernel": [_i64, _i64, ctypes.c_int],
     "linattn_seq_plan": [_i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i64)],
     "linattn_state_pass_segmented": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_int,

@@ -364,6 +364,21 @@ int linattn_decode_step(const void* q, const void* k, const void* v, void* o, fl
                      "decode_step");
 }
 
+int linattn_recurrent(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                      const float* s_in, float* s_out, int64_t B, int64_t H, int64_t N, int64_t dk,
+                      int64_t dv, int dtype, void* stream) {
+  ShapeArgs s{B, H, N, dk, dv};
+  if (int e = check_dims(s, true)) return e;
+  if (int e = check_dtype(dtype)) return e;
+  if (!q || !k || !v || !o || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
+  const int64_t ev = dtype == LINATTN_BF16 ? 8 : 4;
+  if (dv % ev != 0 || dk % ev != 0 || dk > 256)
+    return fail(LINATTN_EUNSUPPORTED, "recurrent kernel needs dk, dv multiples of 16 bytes and dk <= 256 "
+                "(got %lld, %lld)", (long long)dk, (long long)dv);
+  return cuda_status(launch_recurrent(q, k, v, o, log2g, s_in, s_out, s, dtype, (cudaStream_t)stream),
+                     "recurrent");
+}
+
 int linattn_prefill_kernel(int64_t dk, int64_t dv, int dtype) {
   ShapeArgs s{1, 1, 1, dk, dv};
   return tc_supported(s, dtype) ? LINATTN_KERNEL_TC : LINATTN_KERNEL_SIMT;

@@ -105,6 +105,11 @@ cudaError_t launch_state_at(const float* loc, const float* s_in, float* out, con
 bool tc_supported(const ShapeArgs& s, int dtype);
 void set_trace(void* buf);  // debug only: per-chunk clock64 trace of CTA (0,0), nullptr = off
 
+// Whole-sequence row recurrence in one launch (reference _row_based_slice, kernels.py:93-106).
+cudaError_t launch_recurrent(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                             const float* s_in, float* s_out, const ShapeArgs& s, int dtype,
+                             cudaStream_t stream);
+
 cudaError_t launch_decode_step(const void* q, const void* k, const void* v, void* o,
                                float* state, const float* log2g, const ShapeArgs& s,
                                int dtype, cudaStream_t stream);

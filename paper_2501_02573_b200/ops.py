@@ -230,6 +230,19 @@ def decode_step(q, k, v, state, log2g, *, out=None):
     return out
 
 
+def recurrent(q, k, v, log2g, *, s_in=None, s_out=None, out=None):
+    """Row recurrence over whole sequences in one launch (S <- gamma S + k^T v; o = q S)."""
+    _require_cuda(q, k, v, log2g, s_in, s_out, out)
+    B, H, N, dk = q.shape
+    dv = v.shape[3]
+    if out is None:
+        out = torch.empty_like(v)
+    lib = _lib.load()
+    _lib.check(lib.linattn_recurrent(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), log2g.data_ptr(),
+                                     _ptr(s_in), _ptr(s_out), B, H, N, dk, dv, _dtype_code(q), _stream()))
+    return out
+
+
 def prefill_kernel_name(dk: int, dv: int, dtype=torch.bfloat16, kernel: str = "auto") -> str:
     """Which kernel family a prefill of this shape runs ("prefill_tc" or "prefill_simt")."""
     if kernel == "simt":

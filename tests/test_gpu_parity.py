@@ -358,3 +358,23 @@ def test_dk256_lazy_normalisation_regimes(la, decay):
     assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
     ref_s = np.stack([[orc.segment_end_state(c[0, h], v[0, h], gam[h] if decay else 1.0) for h in range(6)]])
     assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= 5e-3
+
+
+@pytest.mark.parametrize("dk,dv,dt", [(128, 128, torch.float32), (64, 256, torch.bfloat16), (256, 128, torch.float32),
+                                      (8, 12, torch.float32)])
+def test_recurrent_scan_kernel(la, dk, dv, dt):
+    """b200-recurrent = the reference row-based route in one launch (kernels.py:93-106)."""
+    from paper_2501_02573_b200 import ops
+    gam = [0.0, 0.93, 1.0]
+    b, c, v = (orc.bf16_round(x) for x in orc.gen_inputs(2, 3, 333, dk, dv, np.float32, 21))
+    ref = orc.oracle_attn(b, c, v, gam, True)
+    out, opc = la.run_method(la.MethodId.B200_RECURRENT, la.make_inputs(dev(b, dt), dev(c, dt), dev(v, dt), gam, True))
+    assert opc > 0
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= (TOL_F32 if dt == torch.float32 else TOL_BF16)
+    # seeded state in / state out continues a sequence exactly like one pass
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    if dv % 4 == 0:
+        s_mid = torch.empty(2, 3, dk, dv, device="cuda")
+        ops.recurrent(dev(b[:, :, :200], dt), dev(c[:, :, :200], dt), dev(v[:, :, :200], dt), l2, s_out=s_mid)
+        tail = ops.recurrent(dev(b[:, :, 200:], dt), dev(c[:, :, 200:], dt), dev(v[:, :, 200:], dt), l2, s_in=s_mid)
+        assert orc.max_rel_error(tail.float().cpu().numpy(), ref[:, :, 200:]) <= (TOL_F32 if dt == torch.float32 else TOL_BF16)
