@@ -165,6 +165,8 @@ def test_host_validation_errors_without_gpu():
         _lib.check(lib.linattn_prefill(1, 1, 1, 1, 1, None, None, 1, 1, 8, 4, 4, 7, 0, None))
     with pytest.raises(la.UsageError, match="tensor-core"):
         _lib.check(lib.linattn_prefill(1, 1, 1, 1, 1, None, None, 1, 1, 8, 4, 4, 0, 1, None))
+    with pytest.raises(la.UsageError, match="65535"):
+        _lib.check(lib.linattn_prefill(1, 1, 1, 1, 1, None, None, 256, 257, 8, 4, 4, 1, 0, None))
     with pytest.raises(la.ParameterError):
         import ctypes
         lens = (ctypes.c_int64 * 2)(1, 2)
