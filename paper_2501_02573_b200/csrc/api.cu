@@ -2,6 +2,7 @@
 // Host-side validation mirrors the reference's typed errors (tensor.py:97-123,
 // errors.py:4-29); every entry point is stream-ordered and never synchronises.
 #include <algorithm>
+#include <cstdlib>
 #include <initializer_list>
 #include <cstdio>
 #include <cstdarg>
@@ -211,6 +212,21 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
       return cuda_status(e, tc ? "prefill_tc (sequence split)" : "prefill_simt (sequence split)");
     }
     cudaGetLastError();  // no workspace: run unsplit
+  }
+  // more units than SMs, not a whole number of waves: one persistent CTA per SM over equal
+  // chunk ranges (sequence heads hand their end state to the next range; LINATTN_NO_BALANCE=1: off)
+  static const bool no_balance = getenv("LINATTN_NO_BALANCE") != nullptr;
+  const int64_t units = s.B * s.H * ceil_div(s.dv, 128);
+  const int ctas = sm_count();
+  if (tc && !no_balance && s.dk <= 128 && units > ctas && units % ctas != 0) {
+    void* ws = nullptr;
+    cudaMemPool_t pool = work_pool();
+    if (pool && cudaMallocFromPoolAsync(&ws, balance_workspace_bytes(s, ctas), pool, st) == cudaSuccess) {
+      cudaError_t e = launch_prefill_tc_balanced(q, k, v, o, log2g, s_in, s_out, s, ctas, ws, st);
+      cudaFreeAsync(ws, st);
+      if (e != cudaErrorNotSupported) return cuda_status(e, "prefill_tc (balanced)");
+    }
+    cudaGetLastError();
   }
   return cuda_status(launch(q, o, s_in, s_out, false, SegArgs{}, 1), what);
 }

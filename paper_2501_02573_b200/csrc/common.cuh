@@ -80,6 +80,66 @@ __device__ __forceinline__ float seg_loc_weight(const SegArgs& sa, int q, int N,
   return gpow(lg, (float)(lo - qhi));
 }
 
+// Balanced persistent schedule (tensor-core kernel, dk <= 128, units >= CTAs): the units x nc
+// chunks of the launch are cut into equal contiguous ranges of w >= nc chunks, one per CTA in
+// ticket order.  A range ends with the HEAD of one sequence and starts with the TAIL of another;
+// the CTA runs the head first and publishes its end state (hst slot t, flags[t]), then whole
+// sequences, then its tail seeded from slot t-1 -- by then the previous CTA has long finished
+// that head, so the hand-off never stalls and every SM streams until the end (no tail wave).
+struct Balance {
+  int on = 0;
+  int units = 0, nc = 0, w = 0, ntiles = 1;
+  float* hst = nullptr;          // [grid][dk][128] fp32 hand-off states
+  unsigned* flags = nullptr;     // [grid] published flags, then the ticket counter (zeroed per launch)
+};
+
+struct WorkItem {
+  int bh, j0, lo, hi;            // unit (batch*head, dv tile) and its token range
+  int in_slot, out_slot;         // hand-off slot to seed from / publish to, -1 = none
+};
+
+__device__ __forceinline__ int balance_items(const Balance& P, int t, long long& start, long long& end) {
+  const long long total = (long long)P.units * P.nc;
+  start = (long long)t * P.w;
+  if (start >= total) return 0;
+  end = min(start + (long long)P.w, total);
+  const int us = (int)(start / P.nc), cs = (int)(start % P.nc);
+  const int ue = (int)(end / P.nc), ce = (int)(end % P.nc);
+  return (ce != 0) + (ue - (cs ? us + 1 : us)) + (cs != 0);
+}
+
+__device__ __forceinline__ WorkItem balance_item(const Balance& P, int N, int t, int k, long long start,
+                                                 long long end) {
+  const int us = (int)(start / P.nc), cs = (int)(start % P.nc);
+  const int ue = (int)(end / P.nc), ce = (int)(end % P.nc);
+  const int f0 = cs ? us + 1 : us;
+  WorkItem w;
+  int u;
+  w.in_slot = -1;
+  w.out_slot = -1;
+  if (ce != 0 && k == 0) {                    // head of unit ue: publish its end state
+    u = ue;
+    w.lo = 0;
+    w.hi = ce * 64;
+    w.out_slot = t;
+  } else {
+    const int kk = k - (ce != 0);
+    if (kk < ue - f0) {                       // whole sequence
+      u = f0 + kk;
+      w.lo = 0;
+      w.hi = N;
+    } else {                                  // tail of unit us, seeded by the previous range's head
+      u = us;
+      w.lo = cs * 64;
+      w.hi = N;
+      w.in_slot = t - 1;
+    }
+  }
+  w.bh = u / P.ntiles;
+  w.j0 = (u % P.ntiles) * 128;
+  return w;
+}
+
 // `nz` = number of (sub-)segments in the launch (grid.z).  In state-only mode s_out receives
 // one local end state per z ([nz][B*H][dk][dv]); otherwise only the last segment writes s_out.
 cudaError_t launch_prefill_simt(const void* q, const void* k, const void* v, void* o,
@@ -103,6 +163,13 @@ cudaError_t launch_segment_prefix(const SegArgs& sa, float* incl, int64_t seg_le
 cudaError_t launch_state_at(const float* loc, const float* s_in, float* out, const SegArgs& sa,
                             int64_t pos, const float* log2g, const ShapeArgs& s, cudaStream_t stream);
 bool tc_supported(const ShapeArgs& s, int dtype);
+
+// Balanced persistent prefill (Balance above): dk in {64, 128}, bf16, B*H*dv-tiles >= ctas.
+// `ws` holds balance_workspace_bytes(s, ctas) bytes (flags are zeroed on the stream here).
+size_t balance_workspace_bytes(const ShapeArgs& s, int ctas);
+cudaError_t launch_prefill_tc_balanced(const void* q, const void* k, const void* v, void* o,
+                                       const float* log2g, const float* s_in, float* s_out,
+                                       const ShapeArgs& s, int ctas, void* ws, cudaStream_t stream);
 void set_trace(void* buf);  // debug only: per-chunk clock64 trace of CTA (0,0), nullptr = off
 
 // Whole-sequence row recurrence in one launch (reference _row_based_slice, kernels.py:93-106).

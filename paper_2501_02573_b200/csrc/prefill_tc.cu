@@ -92,7 +92,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                        const float* __restrict__ log2g, const float* __restrict__ s_in,
                        float* __restrict__ s_out, int H, int N, int dv, int state_only,
-                       const SegArgs sa, unsigned long long* __restrict__ trace) {
+                       const SegArgs sa, const Balance bal, unsigned long long* __restrict__ trace) {
   using G = Cfg<DK, STAGES, SO>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -110,6 +110,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   uint64_t* o_free = mma_o_bar + 2;      // [2] O_intra accumulator b drained     (256 arrivals)
   uint64_t* ox_free = o_free + 2;        // O_inter accumulator drained            (256 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ox_free + 1);
+  int* ticket_slot = reinterpret_cast<int*>(tmem_slot + 1);
   float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);
   uint32_t* pw2 = reinterpret_cast<uint32_t*>(smem + G::OFF_POW2) + 64;   // pw2[k], k in [-64, 127]
   uint8_t* pt_smem = smem + G::OFF_PT;
@@ -117,22 +118,11 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
-  const int bh = blockIdx.y;
-  const int j0 = blockIdx.x * kDVT;
-  int lo, hi;  // this CTA's token segment (SegArgs); boundaries are multiples of kC except N
-  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
-  const int nchunks = hi > lo ? (hi - lo + kC - 1) / kC : 0;
   const size_t per_state = (size_t)gridDim.y * DK * dv;
-  const float lg = log2g[bh % H];
 
-  if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
-  if (threadIdx.x < 192) {
-    const int k = (int)threadIdx.x - 64;
-    const float lo = k >= 0 ? gpow(lg, (float)k) : 0.f;
-    const float hi = k + 1 >= 0 ? gpow(lg, (float)(k + 1)) : 0.f;
-    pw2[k] = pack_bf16x2(lo, hi);
-  }
   if (warp == 12 && lane == 0) {
+    // balanced schedule: tickets in start order, so the range before ours is already running
+    *ticket_slot = bal.on ? (int)atomicAdd(bal.flags + gridDim.x, 1u) : 0;
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -161,8 +151,22 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  // work list: the one unit of blockIdx (SegArgs segment blockIdx.z), or this ticket's range
+  const int ticket = *ticket_slot;
+  long long r_start = 0, r_end = 0;
+  const int nitems = bal.on ? balance_items(bal, ticket, r_start, r_end) : 1;
+  auto item = [&](int k) {
+    if (bal.on) return balance_item(bal, N, ticket, k, r_start, r_end);
+    WorkItem w;
+    w.bh = blockIdx.y;
+    w.j0 = blockIdx.x * kDVT;
+    seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, w.lo, w.hi);  // multiples of kC except N
+    w.in_slot = w.out_slot = -1;
+    return w;
+  };
+  auto item_chunks = [&](const WorkItem& w) { return w.hi > w.lo ? (w.hi - w.lo + kC - 1) / kC : 0; };
   // debug trace of one CTA: (bh = trace[15 * 4096], dv tile 0, segment 0); trace[15 * 4096] is set by the host
-  const bool tracing = trace != nullptr && blockIdx.x == 0 && blockIdx.z == 0 &&
+  const bool tracing = trace != nullptr && !bal.on && blockIdx.x == 0 && blockIdx.z == 0 &&
                        blockIdx.y == (unsigned)trace[15 * 4096];
   const int lin_block = blockIdx.y * gridDim.x + blockIdx.x;
   auto gtime = [] {
@@ -179,13 +183,27 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
   if (warp < 4) {
     // ------------------------------------------------------------ P^T mask / K' scaling
-    for (int c = 0; c < nchunks; ++c) {
-      const int s = c % STAGES;
-      const int b = c & 1;
-      const int L = min(kC, hi - lo - c * kC);
-      mbar_wait(&full[s], (c / STAGES) & 1);
+    int gc = 0;                                     // chunk counter over the whole work list
+    for (int it = 0; it < nitems; ++it) {
+     const WorkItem w = item(it);
+     {
+      // this role's (gamma^k, gamma^(k+1)) table for the item's head, k = -64..127
+      const float lg = log2g[w.bh % H];
+      if (it > 0) named_bar_sync(4, 128);           // every mask thread is done with the old table
+      for (int i = (int)threadIdx.x; i < 192; i += 128) {
+        const int k = i - 64;
+        pw2[k] = pack_bf16x2(k >= 0 ? gpow(lg, (float)k) : 0.f, k + 1 >= 0 ? gpow(lg, (float)(k + 1)) : 0.f);
+      }
+      named_bar_sync(4, 128);
+     }
+     const int nch = item_chunks(w);
+     for (int c = 0; c < nch; ++c, ++gc) {
+      const int s = gc % STAGES;
+      const int b = gc & 1;
+      const int L = min(kC, w.hi - w.lo - c * kC);
+      mbar_wait(&full[s], (gc / STAGES) & 1);
       if (!state_only) {
-        mbar_wait(mma1_bar, c & 1);                 // MMA1 has consumed the unscaled K
+        mbar_wait(mma1_bar, gc & 1);                // MMA1 has consumed the unscaled K
         tc_fence_after();
       }
       if (warp < 2 && !state_only) {
@@ -259,6 +277,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       tc_fence_before();
       if (tracing && lane == 0) trace[(warp < 2 ? 3 : 4) * 4096 + c] = clock64();
       mbar_arrive(&epi1_bar[s]);
+     }
     }
   } else if (warp < 12) {
     // ------------------------------------------------------------ running state + outputs
@@ -268,33 +287,15 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     const int g = (warp - 4) / 4;
     const int sub = (warp - 4) % 4;
     const int d = sub * 32 + lane;
-    const int jd = j0 + d;
-    const bool dv_ok = jd < dv;
     const int col0 = g * SC;
     const uint32_t ta_s = tbase + ((sub * 32) << 16) + T_DS + col0;
     const int d0 = sub * 32 + g * 16;
     const uint32_t ta_o = tbase + ((uint32_t)d0 << 16);
     const bool leader = (warp == 4 && lane == 0);
-    float S[SC];
-    {
-      // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs)
-      const float w_in = gpow(lg, (float)lo);
-#pragma unroll
-      for (int j = 0; j < SC; j += 16) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          S[j + i] = (s_in && dv_ok) ? w_in * s_in[((size_t)bh * DK + col0 + j + i) * dv + jd] : 0.f;
-        for (int qi = 0; qi < sa.nloc; ++qi) {
-          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
-          if (wq < 0.f || !dv_ok) continue;
-          const float* lq = sa.loc + qi * per_state + ((size_t)bh * DK + col0 + j) * dv + jd;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) S[j + i] = fmaf(wq, lq[(size_t)i * dv], S[j + i]);
-        }
-      }
-    }
+    const int sidx = (int)threadIdx.x - 128;     // 0..255 within the role
     // S (fp32 regs) -> bf16 pairs -> TMEM S^T operand buffer `buf` (row d, columns col0/2..)
     const uint32_t ta_st = tbase + ((sub * 32) << 16) + T_ST + col0 / 2;
+    float S[SC];
     auto publish = [&](int buf) {
 #pragma unroll
       for (int j = 0; j < SC / 32; ++j) {
@@ -307,92 +308,141 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       tc_fence_before();
       mbar_arrive(&st_full[buf]);
     };
-    // end state: state-only launches write one local state per segment, full launches only
-    // the last segment (whose seed already covers every earlier token)
-    float* const so = (s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1))
-                          ? s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)bh * DK + col0) * dv + jd
-                          : nullptr;
-#define LA_WRITE_STATE()                                          \
-  do {                                                            \
-    if (so != nullptr) {                                          \
-      _Pragma("unroll") for (int i = 0; i < SC; ++i) so[(size_t)i * dv] = S[i]; \
-    }                                                             \
-  } while (0)
-    if (nchunks == 0) LA_WRITE_STATE();
-    if (!state_only && nchunks > 0) publish(0);
     // stmatrix row address of this thread: matrix m = lane/8 of each x4 group, row lane%8
     const int mrow = lane & 7;
     const int mi = lane >> 3;                  // 0: (d0, t), 1: (d0+8, t), 2: (d0, t+8), 3: (d0+8, t+8)
     const int md = d0 + (mi & 1) * 8;          // 8-aligned dv row of the tile this address serves
-    for (int c = 0; c < nchunks; ++c) {
-      const int L = min(kC, hi - lo - c * kC);
-      const int b = c & 1;
-      mbar_wait(mma_s_bar, c & 1);
-      tc_fence_after();
-      const float carry = pw[L];
+    int gc = 0;
+    for (int it = 0; it < nitems; ++it) {
+      const WorkItem w = item(it);
+      const int jd = w.j0 + d;
+      const bool dv_ok = jd < dv;
+      const float lg = log2g[w.bh % H];
+      // this role's gamma^n table (n = 0..64) for the item's head; a seeded tail also waits here
+      // for the previous range's published head state
+      if (it > 0) named_bar_sync(3, 256);      // every state thread is done with the old table
+      if (sidx <= kC) pw[sidx] = gpow(lg, (float)sidx);
+      if (w.in_slot >= 0 && leader)
+        while (ld_acquire_gpu(bal.flags + w.in_slot) == 0u) __nanosleep(256);
+      named_bar_sync(3, 256);
+      if (w.in_slot >= 0) {
+        // balanced tail: the hand-off state already covers s_in and every earlier token
+        const float* hp = bal.hst + ((size_t)w.in_slot * DK + col0) * kDVT + d;
 #pragma unroll
-      for (int j = 0; j < SC / 16; ++j) {
-        float ds[16];
-        tmem_ld16(ta_s + 16 * j, ds);
-        tmem_wait_ld();
+        for (int i = 0; i < SC; ++i) S[i] = dv_ok ? __ldcg(hp + (size_t)i * kDVT) : 0.f;
+      } else {
+        // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs)
+        const float w_in = gpow(lg, (float)w.lo);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) S[16 * j + i] = fmaf(carry, S[16 * j + i], ds[i]);
-      }
-      tc_fence_before();
-      mbar_arrive(ds_free);
-      if (tracing && lane == 0 && sub == 0 && g == 0) trace[6 * 4096 + c] = clock64();
-      if (c == nchunks - 1) LA_WRITE_STATE();
-      if (state_only) continue;
-      if (c != nchunks - 1) {
-        // buffer (c+1)&1 was last read by Ox_{c-1}, which precedes dS_c in the tensor pipe
-        publish((c + 1) & 1);
-        if (tracing && lane == 0 && sub == 0 && g == 0) trace[7 * 4096 + c] = clock64();
-      }
-      mbar_wait(&mma_o_bar[b], (c >> 1) & 1);    // O_c done
-      tc_fence_after();
-      // ---- outputs of chunk c: O = Oi + gamma^(t+1) Ox (16 lanes x 64 tokens) -> bf16 ->
-      //      smem [t][d] (stmatrix.trans, 128B swizzle) -> TMA bulk store (clips N and dv)
-      uint8_t* ot = ot_smem + (c % G::OT_BUFS) * G::OT_BYTES;
-      if (leader) bulk_wait_read<G::OT_BUFS - 1>();   // the store that last used this tile has read it
-      named_bar_sync(1, 256);
+        for (int j = 0; j < SC; j += 16) {
 #pragma unroll
-      for (int q4 = 0; q4 < 2; ++q4) {           // tokens q4*32 .. q4*32+31
-        uint32_t ro[16], rx[16];
-        tmem_ld_16x256b_x4(ta_o + T_O + b * kC + q4 * 32, ro);
-        tmem_ld_16x256b_x4(ta_o + T_OX + q4 * 32, rx);
-        tmem_wait_ld();
-        if (q4 == 1) {
-          tc_fence_before();
-          mbar_arrive(&o_free[b]);
-          mbar_arrive(ox_free);
-        }
-        uint32_t pk[8];
+          for (int i = 0; i < 16; ++i)
+            S[j + i] = (s_in && dv_ok) ? w_in * s_in[((size_t)w.bh * DK + col0 + j + i) * dv + jd] : 0.f;
+          for (int qi = 0; qi < sa.nloc; ++qi) {
+            const float wq = seg_loc_weight(sa, qi, N, w.lo, lg);
+            if (wq < 0.f || !dv_ok) continue;
+            const float* lq = sa.loc + qi * per_state + ((size_t)w.bh * DK + col0 + j) * dv + jd;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {            // 8-token group r: t = q4*32 + 8r + tq + {0,1}
-          // O = Oi + gamma^(t+1) Ox, in fp32 (the inter-chunk weight, reference w_t kernels.py:125)
-          const int t0 = q4 * 32 + 8 * r + 2 * (lane & 3);
-          const float w0 = pw[t0 + 1], w1 = pw[t0 + 2];
-          pk[2 * r + 0] = pack_bf16x2(fmaf(w0, __uint_as_float(rx[4 * r + 0]), __uint_as_float(ro[4 * r + 0])),
-                                      fmaf(w1, __uint_as_float(rx[4 * r + 1]), __uint_as_float(ro[4 * r + 1])));
-          pk[2 * r + 1] = pack_bf16x2(fmaf(w0, __uint_as_float(rx[4 * r + 2]), __uint_as_float(ro[4 * r + 2])),
-                                      fmaf(w1, __uint_as_float(rx[4 * r + 3]), __uint_as_float(ro[4 * r + 3])));
-        }
-#pragma unroll
-        for (int rr = 0; rr < 4; rr += 2) {      // two 8-token groups per stmatrix.x4
-          const int tt = q4 * 32 + rr * 8 + (mi >> 1) * 8 + mrow;     // token row this lane addresses
-          const uint32_t addr = smem_u32(ot + (md / 64) * (kC * 128) + tt * 128 +
-                                         ((((md % 64) >> 3) ^ (tt & 7)) << 4));
-          stmatrix_x4_trans(addr, pk[2 * rr + 0], pk[2 * rr + 1], pk[2 * rr + 2], pk[2 * rr + 3]);
+            for (int i = 0; i < 16; ++i) S[j + i] = fmaf(wq, lq[(size_t)i * dv], S[j + i]);
+          }
         }
       }
-      fence_proxy_async_smem();
-      named_bar_sync(2, 256);
-      if (leader) {
-        tma_store_3d(&tm_o, ot, j0, lo + c * kC, bh);
-        tma_store_3d(&tm_o, ot + kC * 128, j0 + 64, lo + c * kC, bh);
-        bulk_commit();
+      // end state: a balanced head publishes to its hand-off slot; otherwise state-only launches
+      // write one local state per segment, full launches only the segment ending the sequence
+      // (whose seed already covers every earlier token)
+      float* so = nullptr;
+      size_t so_stride = dv;
+      if (w.out_slot >= 0) {
+        if (dv_ok) so = bal.hst + ((size_t)w.out_slot * DK + col0) * kDVT + d;
+        so_stride = kDVT;
+      } else if (s_out && dv_ok &&
+                 (bal.on ? w.hi == N : (state_only || blockIdx.z == gridDim.z - 1))) {
+        so = s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)w.bh * DK + col0) * dv + jd;
       }
-      if (tracing && lane == 0 && sub == 0 && g == 0) trace[5 * 4096 + c] = clock64();
+      auto write_state = [&]() {
+        if (so != nullptr) {
+#pragma unroll
+          for (int i = 0; i < SC; ++i) so[(size_t)i * so_stride] = S[i];
+        }
+        if (w.out_slot >= 0) {                 // release the hand-off to the next range's tail
+          __threadfence();
+          named_bar_sync(5, 256);
+          if (leader) st_release_gpu(bal.flags + w.out_slot, 1u);
+        }
+      };
+      const int nch = item_chunks(w);
+      if (nch == 0) write_state();
+      if (!state_only && nch > 0) publish(gc & 1);
+      for (int c = 0; c < nch; ++c, ++gc) {
+        const int L = min(kC, w.hi - w.lo - c * kC);
+        const int b = gc & 1;
+        mbar_wait(mma_s_bar, gc & 1);
+        tc_fence_after();
+        const float carry = pw[L];
+#pragma unroll
+        for (int j = 0; j < SC / 16; ++j) {
+          float ds[16];
+          tmem_ld16(ta_s + 16 * j, ds);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) S[16 * j + i] = fmaf(carry, S[16 * j + i], ds[i]);
+        }
+        tc_fence_before();
+        mbar_arrive(ds_free);
+        if (tracing && lane == 0 && sub == 0 && g == 0) trace[6 * 4096 + c] = clock64();
+        if (c == nch - 1) write_state();
+        if (state_only) continue;
+        if (c != nch - 1) {
+          // buffer (gc+1)&1 was last read by Ox_{gc-1}, which precedes dS_gc in the tensor pipe
+          publish((gc + 1) & 1);
+          if (tracing && lane == 0 && sub == 0 && g == 0) trace[7 * 4096 + c] = clock64();
+        }
+        mbar_wait(&mma_o_bar[b], (gc >> 1) & 1);   // O_gc done
+        tc_fence_after();
+        // ---- outputs of chunk c: O = Oi + gamma^(t+1) Ox (16 lanes x 64 tokens) -> bf16 ->
+        //      smem [t][d] (stmatrix.trans, 128B swizzle) -> TMA bulk store (clips N and dv)
+        uint8_t* ot = ot_smem + (gc % G::OT_BUFS) * G::OT_BYTES;
+        if (leader) bulk_wait_read<G::OT_BUFS - 1>();   // the store that last used this tile has read it
+        named_bar_sync(1, 256);
+#pragma unroll
+        for (int q4 = 0; q4 < 2; ++q4) {           // tokens q4*32 .. q4*32+31
+          uint32_t ro[16], rx[16];
+          tmem_ld_16x256b_x4(ta_o + T_O + b * kC + q4 * 32, ro);
+          tmem_ld_16x256b_x4(ta_o + T_OX + q4 * 32, rx);
+          tmem_wait_ld();
+          if (q4 == 1) {
+            tc_fence_before();
+            mbar_arrive(&o_free[b]);
+            mbar_arrive(ox_free);
+          }
+          uint32_t pk[8];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {            // 8-token group r: t = q4*32 + 8r + tq + {0,1}
+            // O = Oi + gamma^(t+1) Ox, in fp32 (the inter-chunk weight, reference w_t kernels.py:125)
+            const int t0 = q4 * 32 + 8 * r + 2 * (lane & 3);
+            const float w0 = pw[t0 + 1], w1 = pw[t0 + 2];
+            pk[2 * r + 0] = pack_bf16x2(fmaf(w0, __uint_as_float(rx[4 * r + 0]), __uint_as_float(ro[4 * r + 0])),
+                                        fmaf(w1, __uint_as_float(rx[4 * r + 1]), __uint_as_float(ro[4 * r + 1])));
+            pk[2 * r + 1] = pack_bf16x2(fmaf(w0, __uint_as_float(rx[4 * r + 2]), __uint_as_float(ro[4 * r + 2])),
+                                        fmaf(w1, __uint_as_float(rx[4 * r + 3]), __uint_as_float(ro[4 * r + 3])));
+          }
+#pragma unroll
+          for (int rr = 0; rr < 4; rr += 2) {      // two 8-token groups per stmatrix.x4
+            const int tt = q4 * 32 + rr * 8 + (mi >> 1) * 8 + mrow;     // token row this lane addresses
+            const uint32_t addr = smem_u32(ot + (md / 64) * (kC * 128) + tt * 128 +
+                                           ((((md % 64) >> 3) ^ (tt & 7)) << 4));
+            stmatrix_x4_trans(addr, pk[2 * rr + 0], pk[2 * rr + 1], pk[2 * rr + 2], pk[2 * rr + 3]);
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(2, 256);
+        if (leader) {
+          tma_store_3d(&tm_o, ot, w.j0, w.lo + c * kC, w.bh);
+          tma_store_3d(&tm_o, ot + kC * 128, w.j0 + 64, w.lo + c * kC, w.bh);
+          bulk_commit();
+        }
+        if (tracing && lane == 0 && sub == 0 && g == 0) trace[5 * 4096 + c] = clock64();
+      }
     }
     if (leader) bulk_wait<0>();
   } else {
@@ -400,21 +450,26 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       // ---------------------------------------------------------- TMA producer
       if (lane == 0) {
         const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES + G::V_BYTES;
-        for (int c = 0; c < nchunks; ++c) {
-          const int s = c % STAGES;
-          mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
-          if (tracing) trace[13 * 4096 + c] = clock64();
-          uint8_t* st = smem + s * G::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[s], bytes);
+        int gc = 0;
+        for (int it = 0; it < nitems; ++it) {
+          const WorkItem w = item(it);
+          const int nch = item_chunks(w);
+          for (int c = 0; c < nch; ++c, ++gc) {
+            const int s = gc % STAGES;
+            const int t0 = w.lo + c * kC;
+            mbar_wait(&empty[s], ((gc / STAGES) & 1) ^ 1);
+            if (tracing) trace[13 * 4096 + c] = clock64();
+            uint8_t* st = smem + s * G::STAGE_BYTES;
+            mbar_arrive_expect_tx(&full[s], bytes);
 #pragma unroll
-          for (int kb = 0; kb < G::KB; ++kb) {
-            if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);
-            tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh);
+            for (int kb = 0; kb < G::KB; ++kb) {
+              if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, t0, w.bh);
+              tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, t0, w.bh);
+            }
+#pragma unroll
+            for (int nb = 0; nb < kDVT / 64; ++nb)
+              tma_load_3d(st + G::Q_BYTES + G::K_BYTES + nb * 8192, &tm_v, &full[s], w.j0 + nb * 64, t0, w.bh);
           }
-#pragma unroll
-          for (int nb = 0; nb < kDVT / 64; ++nb)
-            tma_load_3d(st + G::Q_BYTES + G::K_BYTES + nb * 8192, &tm_v, &full[s], j0 + nb * 64,
-                        lo + c * kC, bh);
         }
       }
     } else if (warp == 13) {
@@ -445,6 +500,9 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         mma_commit_elect(mma1_bar);
         if (tracing && lane == 0) trace[11 * 4096 + c] = clock64();
       };
+      // the tensor pipe sees one flat chunk stream across the work list (c counts every chunk)
+      int nchunks = 0;
+      for (int it = 0; it < nitems; ++it) nchunks += item_chunks(item(it));
       if (!state_only && nchunks > 0) issue_mma1(0);
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % STAGES;
@@ -1058,7 +1116,8 @@ bool make_map(CUtensorMap* map, const void* base, int64_t D, int64_t N, int64_t 
 template <int DK, int STAGES, bool SO = false>
 cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, const float* log2g,
                         const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
-                        const SegArgs& sa, int nz, cudaStream_t stream) {
+                        const SegArgs& sa, int nz, cudaStream_t stream, const Balance& bal = Balance{},
+                        int ctas = 0) {
   using G = v2::Cfg<DK, STAGES, SO>;
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
   CUtensorMap mq, mk, mv;
@@ -1074,10 +1133,11 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   auto kern = v2::prefill_tc_pipe_kernel<DK, STAGES, SO>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
-  dim3 grid((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
+  const dim3 grid = bal.on ? dim3((unsigned)ctas)
+                           : dim3((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
   kern<<<grid, v2::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out,
                                                 (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
-                                                sa, g_trace);
+                                                sa, bal, g_trace);
   count_launch();
   return cudaGetLastError();
 }
@@ -1166,6 +1226,35 @@ cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void*
     case 256: return launch_tmem_state<256, 2>(q, k, v, o, log2g, s_in, s_out, s, state_only, sa, nz, stream);
     default: return cudaErrorNotSupported;
   }
+}
+
+size_t balance_workspace_bytes(const ShapeArgs& s, int ctas) {
+  return 256 * (size_t)((ctas + 1 + 63) / 64) + (size_t)ctas * s.dk * kDVT * sizeof(float);
+}
+
+cudaError_t launch_prefill_tc_balanced(const void* q, const void* k, const void* v, void* o,
+                                       const float* log2g, const float* s_in, float* s_out,
+                                       const ShapeArgs& s, int ctas, void* ws, cudaStream_t stream) {
+  for (const void* p : {q, k, v, (const void*)o})
+    if (reinterpret_cast<uintptr_t>(p) & 15) return cudaErrorNotSupported;
+  const int64_t ntiles = (s.dv + kDVT - 1) / kDVT;
+  const int64_t units = s.B * s.H * ntiles, nc = (s.N + kC - 1) / kC;
+  const int64_t w = (units * nc + ctas - 1) / ctas;
+  if ((s.dk != 64 && s.dk != 128) || w < nc || units * nc > (1LL << 31) - 1) return cudaErrorNotSupported;
+  Balance bal;
+  bal.on = 1;
+  bal.units = (int)units;
+  bal.nc = (int)nc;
+  bal.w = (int)w;
+  bal.ntiles = (int)ntiles;
+  bal.flags = static_cast<unsigned*>(ws);
+  bal.hst = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256 * (size_t)((ctas + 1 + 63) / 64));
+  const int used = (int)((units * nc + w - 1) / w);     // ranges that hold work
+  cudaError_t err = cudaMemsetAsync(ws, 0, sizeof(unsigned) * (ctas + 1), stream);
+  if (err != cudaSuccess) return err;
+  if (s.dk == 64)
+    return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, false, SegArgs{}, 1, stream, bal, used);
+  return launch_pipe<128, V2_STAGES128>(q, k, v, o, log2g, s_in, s_out, s, false, SegArgs{}, 1, stream, bal, used);
 }
 
 }  // namespace linattn

@@ -205,3 +205,28 @@ def test_long_context_gamma_near_one(ops):
         ref, _ = orc.seeded_blocked_attn(qq[None, None], kk[None, None, N - T:], vv[None, None, N - T:],
                                          [gam[h]], True, s_pre[None, None], block=64)
         assert orc.max_rel_error(o[0, h, N - T:].float().cpu().numpy(), ref[0, 0]) <= TOL_BF16
+
+
+@pytest.mark.parametrize("B,H,dk,dv", [(2, 80, 128, 128), (1, 75, 64, 256), (3, 53, 128, 192)])
+@pytest.mark.parametrize("N", [1, 64, 200, 1000])
+def test_balanced_schedule(ops, B, H, dk, dv, N):
+    """More units than SMs (not a whole number of waves) runs the balanced persistent schedule:
+    sequence heads publish their end state to the next CTA's range.  Checked with s_in seeding
+    and s_out against the seeded f64 blocked oracle, gamma in {0, 1} included."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    units = B * H * -(-dv // 128)
+    assert units > sms and units % sms != 0           # the balanced path is the one under test
+    gam = [0.0, 1.0] + [1 - 2.0 ** (-3 - (h % 12)) for h in range(H - 2)]
+    b, c, v = orc.gen_inputs(B, H, N, dk, dv, np.float32, 40 + N)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    s0 = np.random.default_rng(N).standard_normal((B, H, dk, dv)).astype(np.float32) * 0.05
+    ref, ref_s = orc.seeded_blocked_attn(b, c, v, gam, True, s0.astype(np.float64), block=64)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    q, k, vv = dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16)
+    s_out = torch.full((B, H, dk, dv), float("nan"), device="cuda")
+    out = ops.prefill(q, k, vv, l2, s_in=dev(s0), s_out=s_out)
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
+    assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= 5e-3
+    # repeated launches reuse the pooled workspace (flags re-zeroed per launch)
+    again = ops.prefill(q, k, vv, l2, s_in=dev(s0))
+    assert torch.equal(again, out)

@@ -21,6 +21,8 @@ CFGS = {
     "cfg3": (4, 16, 16384, 256, 512),
     "cfg5": (1, 32, 131072, 128, 128),
     "cfg2s": (2, 32, 8192, 128, 128),
+    "cfg2x": (5, 32, 8192, 128, 128),      # 160 units: 1.08 waves unbalanced
+    "cfg2d": (8, 32, 8192, 64, 128),
 }
 
 

@@ -53,4 +53,5 @@ def main(mode="full", B=8, H=32, N=8192, d=128, cta=0):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "full", cta=int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    shape = dict(zip("BHN", map(int, sys.argv[3].split(",")))) if len(sys.argv) > 3 else {}
+    main(sys.argv[1] if len(sys.argv) > 1 else "full", cta=int(sys.argv[2]) if len(sys.argv) > 2 else 0, **shape)
