@@ -213,12 +213,17 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
     }
     cudaGetLastError();  // no workspace: run unsplit
   }
-  // more units than SMs, not a whole number of waves: one persistent CTA per SM over equal
-  // chunk ranges (sequence heads hand their end state to the next range; LINATTN_NO_BALANCE=1: off)
-  static const bool no_balance = getenv("LINATTN_NO_BALANCE") != nullptr;
+  // more units than SMs and a mostly empty last wave: one persistent CTA per SM over equal chunk
+  // ranges (sequence heads hand their end state to the next range).  A last wave more than half
+  // full already streams near the HBM roofline (each CTA is bound by its own serial chunk chain,
+  // so fewer CTAs each go faster), and there the plain grid is kept.
+  // LINATTN_BALANCE=0 / 1: never / whenever the units are not a whole number of waves (dev A/B).
+  static const int balance_env = getenv("LINATTN_BALANCE") ? atoi(getenv("LINATTN_BALANCE")) : -1;
   const int64_t units = s.B * s.H * ceil_div(s.dv, 128);
   const int ctas = sm_count();
-  if (tc && !no_balance && s.dk <= 128 && units > ctas && units % ctas != 0) {
+  const int64_t rem = units % ctas;
+  const bool balance = balance_env < 0 ? (rem != 0 && 2 * rem <= ctas) : (balance_env > 0 && rem != 0);
+  if (tc && balance && s.dk <= 128 && units > ctas) {
     void* ws = nullptr;
     cudaMemPool_t pool = work_pool();
     if (pool && cudaMallocFromPoolAsync(&ws, balance_workspace_bytes(s, ctas), pool, st) == cudaSuccess) {

@@ -86,7 +86,9 @@ __device__ __forceinline__ uint32_t hmul2_bf16(uint32_t a, uint32_t b) {
   return r;
 }
 
-template <int DK, int STAGES, bool SO>
+// BAL: balanced persistent work list (Balance); false = one unit per CTA from blockIdx, where
+// every item field is a compile-time-known function of blockIdx (no extra live registers).
+template <int DK, int STAGES, bool SO, bool BAL>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -110,7 +112,9 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   uint64_t* o_free = mma_o_bar + 2;      // [2] O_intra accumulator b drained     (256 arrivals)
   uint64_t* ox_free = o_free + 2;        // O_inter accumulator drained            (256 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ox_free + 1);
-  int* ticket_slot = reinterpret_cast<int*>(tmem_slot + 1);
+  // work-list header {ticket, items, range start, range end}: re-read from shared memory at each
+  // item boundary so none of it stays live in registers across the chunk loops
+  int* wl = reinterpret_cast<int*>(tmem_slot + 2);
   float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);
   uint32_t* pw2 = reinterpret_cast<uint32_t*>(smem + G::OFF_POW2) + 64;   // pw2[k], k in [-64, 127]
   uint8_t* pt_smem = smem + G::OFF_PT;
@@ -122,7 +126,16 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
   if (warp == 12 && lane == 0) {
     // balanced schedule: tickets in start order, so the range before ours is already running
-    *ticket_slot = bal.on ? (int)atomicAdd(bal.flags + gridDim.x, 1u) : 0;
+    if constexpr (BAL) {
+      const int t = (int)atomicAdd(bal.flags + gridDim.x, 1u);
+      long long r0 = 0, r1 = 0;
+      wl[1] = balance_items(bal, t, r0, r1);
+      wl[0] = t;
+      reinterpret_cast<long long*>(wl)[1] = r0;
+      reinterpret_cast<long long*>(wl)[2] = r1;
+    } else {
+      wl[1] = 1;
+    }
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -152,11 +165,13 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   // work list: the one unit of blockIdx (SegArgs segment blockIdx.z), or this ticket's range
-  const int ticket = *ticket_slot;
-  long long r_start = 0, r_end = 0;
-  const int nitems = bal.on ? balance_items(bal, ticket, r_start, r_end) : 1;
+  const int nitems = BAL ? wl[1] : 1;
   auto item = [&](int k) {
-    if (bal.on) return balance_item(bal, N, ticket, k, r_start, r_end);
+    if constexpr (BAL) {
+      const volatile int* v = wl;
+      const volatile long long* r = reinterpret_cast<const volatile long long*>(wl);
+      return balance_item(bal, N, v[0], k, r[1], r[2]);
+    }
     WorkItem w;
     w.bh = blockIdx.y;
     w.j0 = blockIdx.x * kDVT;
@@ -166,7 +181,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   };
   auto item_chunks = [&](const WorkItem& w) { return w.hi > w.lo ? (w.hi - w.lo + kC - 1) / kC : 0; };
   // debug trace of one CTA: (bh = trace[15 * 4096], dv tile 0, segment 0); trace[15 * 4096] is set by the host
-  const bool tracing = trace != nullptr && !bal.on && blockIdx.x == 0 && blockIdx.z == 0 &&
+  const bool tracing = trace != nullptr && !BAL && blockIdx.x == 0 && blockIdx.z == 0 &&
                        blockIdx.y == (unsigned)trace[15 * 4096];
   const int lin_block = blockIdx.y * gridDim.x + blockIdx.x;
   auto gtime = [] {
@@ -347,31 +362,29 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
           }
         }
       }
-      // end state: a balanced head publishes to its hand-off slot; otherwise state-only launches
-      // write one local state per segment, full launches only the segment ending the sequence
-      // (whose seed already covers every earlier token)
-      float* so = nullptr;
-      size_t so_stride = dv;
-      if (w.out_slot >= 0) {
-        if (dv_ok) so = bal.hst + ((size_t)w.out_slot * DK + col0) * kDVT + d;
-        so_stride = kDVT;
-      } else if (s_out && dv_ok &&
-                 (bal.on ? w.hi == N : (state_only || blockIdx.z == gridDim.z - 1))) {
-        so = s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)w.bh * DK + col0) * dv + jd;
-      }
-      auto write_state = [&]() {
-        if (so != nullptr) {
-#pragma unroll
-          for (int i = 0; i < SC; ++i) so[(size_t)i * so_stride] = S[i];
-        }
-        if (w.out_slot >= 0) {                 // release the hand-off to the next range's tail
-          __threadfence();
-          named_bar_sync(5, 256);
-          if (leader) st_release_gpu(bal.flags + w.out_slot, 1u);
-        }
-      };
+      // end state (written after the last chunk): a balanced head publishes it to its hand-off
+      // slot; otherwise state-only launches write one local state per segment and full launches
+      // only the segment ending the sequence (whose seed already covers every earlier token)
+#define LA_WRITE_STATE()                                                                              \
+  do {                                                                                                \
+    float* so = nullptr;                                                                              \
+    size_t so_stride = dv;                                                                            \
+    if (w.out_slot >= 0) {                                                                            \
+      if (dv_ok) so = bal.hst + ((size_t)w.out_slot * DK + col0) * kDVT + d;                          \
+      so_stride = kDVT;                                                                               \
+    } else if (s_out && dv_ok && (BAL ? w.hi == N : (state_only || blockIdx.z == gridDim.z - 1))) { \
+      so = s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)w.bh * DK + col0) * dv + jd;  \
+    }                                                                                                 \
+    if (so != nullptr) {                                                                              \
+      _Pragma("unroll") for (int i = 0; i < SC; ++i) so[(size_t)i * so_stride] = S[i];                \
+    }                                                                                                 \
+    if (w.out_slot >= 0) { /* release the hand-off to the next range's tail */                       \
+      __threadfence();                                                                                \
+      named_bar_sync(5, 256);                                                                         \
+      if (leader) st_release_gpu(bal.flags + w.out_slot, 1u);                                         \
+    }                                                                                                 \
+  } while (0)
       const int nch = item_chunks(w);
-      if (nch == 0) write_state();
       if (!state_only && nch > 0) publish(gc & 1);
       for (int c = 0; c < nch; ++c, ++gc) {
         const int L = min(kC, w.hi - w.lo - c * kC);
@@ -390,7 +403,6 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         tc_fence_before();
         mbar_arrive(ds_free);
         if (tracing && lane == 0 && sub == 0 && g == 0) trace[6 * 4096 + c] = clock64();
-        if (c == nch - 1) write_state();
         if (state_only) continue;
         if (c != nch - 1) {
           // buffer (gc+1)&1 was last read by Ox_{gc-1}, which precedes dS_gc in the tensor pipe
@@ -443,6 +455,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         }
         if (tracing && lane == 0 && sub == 0 && g == 0) trace[5 * 4096 + c] = clock64();
       }
+      LA_WRITE_STATE();
     }
     if (leader) bulk_wait<0>();
   } else {
@@ -1130,7 +1143,7 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   }
   CUtensorMap mo = mk;
   if (!state_only && !make_map(&mo, o, s.dv, s.N, BH)) return cudaErrorInvalidValue;
-  auto kern = v2::prefill_tc_pipe_kernel<DK, STAGES, SO>;
+  auto kern = bal.on ? v2::prefill_tc_pipe_kernel<DK, STAGES, SO, true> : v2::prefill_tc_pipe_kernel<DK, STAGES, SO, false>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
   const dim3 grid = bal.on ? dim3((unsigned)ctas)

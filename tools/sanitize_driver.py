@@ -20,5 +20,14 @@ for (B, H, N, dk, dv) in [(1, 2, 300, 128, 128), (1, 1, 200, 64, 64), (1, 1, 130
     st = torch.zeros(B, H, dk, dv, device="cuda")
     ops.decode_step(q[:, :, 0].contiguous(), k[:, :, 0].contiguous(), v[:, :, 0].contiguous(), st, l2)
     ops.prefix_combine(torch.stack([s_out, s_out]), [N, N], 1, l2)
+# more units than SMs: the balanced persistent schedule (head -> tail state hand-off)
+H = torch.cuda.get_device_properties(0).multi_processor_count + 5
+for dk in (128, 64):
+    q = torch.randn(1, H, 300, dk, device="cuda", dtype=torch.bfloat16)
+    k = torch.randn_like(q)
+    v = torch.randn(1, H, 300, 128, device="cuda", dtype=torch.bfloat16)
+    l2 = ops.log2_gamma([0.9] * H, True, "cuda")
+    ops.prefill(q, k, v, l2, s_in=torch.zeros(1, H, dk, 128, device="cuda"),
+                s_out=torch.empty(1, H, dk, 128, device="cuda"))
 torch.cuda.synchronize()
 print("sanitize driver done")
