@@ -3,6 +3,8 @@
 // evaluated as the scan acc <- gamma^(L_q) acc + S_q over q = 0 .. rank-1 (the
 // recursion cross-term weights of the reference, kernels.py:185-189, applied
 // across sequence segments).  Elementwise over [B, H, dk, dv]; float4 accesses.
+// Every scan here batches its loads kLoads entries ahead: with one load in flight per thread
+// these small kernels were DRAM-latency bound (ncu: 8 us for 8-15 MB).
 #include <algorithm>
 
 #include "common.cuh"
@@ -11,6 +13,7 @@ namespace linattn {
 namespace {
 
 constexpr int MAXP = 64;
+constexpr int kLoads = 8;          // entries loaded ahead per thread
 struct SegLens {
   float len[MAXP];
 };
@@ -23,13 +26,20 @@ __global__ void prefix_combine_kernel(const float4* __restrict__ gathered, float
   const int h = (int)((idx / per_head4) % H);
   const float lg = log2g[h];
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int p = 0; p < rank; ++p) {
-    const float c = gpow(lg, lens.len[p]);
-    const float4 x = gathered[(int64_t)p * per_rank4 + idx];
-    acc.x = fmaf(c, acc.x, x.x);
-    acc.y = fmaf(c, acc.y, x.y);
-    acc.z = fmaf(c, acc.z, x.z);
-    acc.w = fmaf(c, acc.w, x.w);
+  for (int p0 = 0; p0 < rank; p0 += kLoads) {
+    float4 x[kLoads];
+#pragma unroll
+    for (int j = 0; j < kLoads; ++j)
+      if (p0 + j < rank) x[j] = gathered[(int64_t)(p0 + j) * per_rank4 + idx];
+#pragma unroll
+    for (int j = 0; j < kLoads; ++j) {
+      if (p0 + j >= rank) break;
+      const float c = gpow(lg, lens.len[p0 + j]);
+      acc.x = fmaf(c, acc.x, x[j].x);
+      acc.y = fmaf(c, acc.y, x[j].y);
+      acc.z = fmaf(c, acc.z, x[j].z);
+      acc.w = fmaf(c, acc.w, x[j].w);
+    }
   }
   s_in[idx] = acc;
 }
@@ -42,7 +52,15 @@ __global__ void prefix_combine_kernel_scalar(const float* __restrict__ gathered,
   const int h = (int)((idx / per_head) % H);
   const float lg = log2g[h];
   float acc = 0.f;
-  for (int p = 0; p < rank; ++p) acc = fmaf(gpow(lg, lens.len[p]), acc, gathered[(int64_t)p * per_rank + idx]);
+  for (int p0 = 0; p0 < rank; p0 += kLoads) {
+    float x[kLoads];
+#pragma unroll
+    for (int j = 0; j < kLoads; ++j)
+      if (p0 + j < rank) x[j] = gathered[(int64_t)(p0 + j) * per_rank + idx];
+#pragma unroll
+    for (int j = 0; j < kLoads; ++j)
+      if (p0 + j < rank) acc = fmaf(gpow(lg, lens.len[p0 + j]), acc, x[j]);
+  }
   s_in[idx] = acc;
 }
 
@@ -60,14 +78,22 @@ __global__ void state_at_kernel(const float4* __restrict__ loc, const float4* __
     const float4 x = s_in[idx];
     acc = make_float4(w * x.x, w * x.y, w * x.z, w * x.w);
   }
-  for (int q = 0; q < sa.nloc; ++q) {
-    const float w = seg_loc_weight(sa, q, N, pos, lg);
-    if (w < 0.f) continue;
-    const float4 x = loc[(int64_t)q * per_state4 + idx];
-    acc.x = fmaf(w, x.x, acc.x);
-    acc.y = fmaf(w, x.y, acc.y);
-    acc.z = fmaf(w, x.z, acc.z);
-    acc.w = fmaf(w, x.w, acc.w);
+  for (int q0 = 0; q0 < sa.nloc; q0 += kLoads) {
+    float4 x[kLoads];
+    float w[kLoads];
+#pragma unroll
+    for (int j = 0; j < kLoads; ++j) {
+      w[j] = q0 + j < sa.nloc ? seg_loc_weight(sa, q0 + j, N, pos, lg) : -1.f;
+      if (w[j] >= 0.f) x[j] = loc[(int64_t)(q0 + j) * per_state4 + idx];
+    }
+#pragma unroll
+    for (int j = 0; j < kLoads; ++j) {
+      if (w[j] < 0.f) continue;
+      acc.x = fmaf(w[j], x[j].x, acc.x);
+      acc.y = fmaf(w[j], x[j].y, acc.y);
+      acc.z = fmaf(w[j], x[j].z, acc.z);
+      acc.w = fmaf(w[j], x[j].w, acc.w);
+    }
   }
   out[idx] = acc;
 }
@@ -82,22 +108,35 @@ __global__ void segment_prefix_kernel(const float4* __restrict__ loc, float4* __
   if (idx >= per_state4) return;
   const float lg = log2g[(int)((idx / per_head4) % H)];
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  int pos = 0, q = 0;
-  for (int p = 0; p < nseg; ++p) {
-    const int hp = (int)min((long long)(p + 1) * seg_len, (long long)N);
-    for (; q < sa.nloc; ++q) {
-      int qlo, qhi;
-      seg_bounds(sa.loc_seg_len, sa.loc_sub, sa.loc_m, q, N, qlo, qhi);
-      if (qhi > hp) break;
-      if (qhi <= qlo) continue;                         // empty sub-segment
-      const float w = gpow(lg, (float)(qhi - pos));
-      const float4 x = loc[(int64_t)q * per_state4 + idx];
-      acc = make_float4(fmaf(w, acc.x, x.x), fmaf(w, acc.y, x.y), fmaf(w, acc.z, x.z), fmaf(w, acc.w, x.w));
-      pos = qhi;
+  int pos = 0, p = 0;
+  auto seg_end = [&](int pp) { return (int)min((long long)(pp + 1) * seg_len, (long long)N); };
+  auto emit = [&](int pp) {        // incl[pp] = state at its segment end, from the state at pos
+    const float w = gpow(lg, (float)(seg_end(pp) - pos));
+    incl[(int64_t)pp * per_state4 + idx] = make_float4(w * acc.x, w * acc.y, w * acc.z, w * acc.w);
+  };
+  // entries in token order; before folding entry q, emit every segment ending before it
+  for (int q0 = 0; q0 < sa.nloc; q0 += kLoads) {
+    float4 x[kLoads];
+    int qhi[kLoads];
+#pragma unroll
+    for (int j = 0; j < kLoads; ++j) {
+      int qlo = 0;
+      qhi[j] = 0;
+      if (q0 + j < sa.nloc) seg_bounds(sa.loc_seg_len, sa.loc_sub, sa.loc_m, q0 + j, N, qlo, qhi[j]);
+      if (qhi[j] <= qlo) qhi[j] = -1;                    // past the end or an empty sub-segment
+      else x[j] = loc[(int64_t)(q0 + j) * per_state4 + idx];
     }
-    const float w = gpow(lg, (float)(hp - pos));
-    incl[(int64_t)p * per_state4 + idx] = make_float4(w * acc.x, w * acc.y, w * acc.z, w * acc.w);
+#pragma unroll
+    for (int j = 0; j < kLoads; ++j) {
+      if (qhi[j] < 0) continue;
+      for (; p < nseg && seg_end(p) < qhi[j]; ++p) emit(p);
+      const float w = gpow(lg, (float)(qhi[j] - pos));
+      acc = make_float4(fmaf(w, acc.x, x[j].x), fmaf(w, acc.y, x[j].y), fmaf(w, acc.z, x[j].z),
+                        fmaf(w, acc.w, x[j].w));
+      pos = qhi[j];
+    }
   }
+  for (; p < nseg; ++p) emit(p);
 }
 
 }  // namespace
