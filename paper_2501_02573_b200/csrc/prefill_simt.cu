@@ -131,18 +131,31 @@ prefill_simt_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* _
 //   O  (CH x 64, over CH + dk): 2 (t) x 4 (j) tile
 //   S  (dk x 64, over CH):   8 (i) x 4 (j) tile, read-modify-write of the smem state
 // Same chunking, masks, decay weights and summation split as prefill_simt_kernel.
-template <typename T>
+// ASYNC (fp32 inputs, 16-byte aligned rows): the next chunk's K and V stream into a second
+// buffer by cp.async while the current chunk computes, and the next Q into the single Q buffer
+// once the output products are done with it -- the synchronous loads left the kernel stalled
+// on global memory (ncu: long-scoreboard half of all issue cycles).
+__device__ __forceinline__ void cp_async16_zfill(float* dst, const float* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <typename T, bool ASYNC>
 __global__ void __launch_bounds__(NT)
 prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
                        T* __restrict__ o, const float* __restrict__ log2g,
                        const float* __restrict__ s_in, float* __restrict__ s_out,
                        int H, int N, int dk, int dv, int state_only, const SegArgs sa) {
+  static_assert(!ASYNC || sizeof(T) == 4, "cp.async staging copies fp32 rows");
   extern __shared__ __align__(16) float smem[];
   const int ld = dk + 4;                      // 16-byte rows, bank-spread
+  constexpr int NB = ASYNC ? 2 : 1;           // K/V buffers
   float* Qs = smem;                           // [CH][ld]
-  float* Ks = Qs + CH * ld;                   // [CH][ld]
-  float* Vs = Ks + CH * ld;                   // [CH][DVT]
-  float* A = Vs + CH * DVT;                   // [CH][CH+4]
+  float* Ks = Qs + CH * ld;                   // [NB][CH][ld]
+  float* Vs = Ks + NB * CH * ld;              // [NB][CH][DVT]
+  float* A = Vs + NB * CH * DVT;              // [CH][CH+4]
   float* S = A + CH * (CH + 4);               // [dk][DVT]
   float* w = S + (size_t)dk * DVT;            // [CH] gamma^(L-1-s)
   float* gq = w + CH;                         // [CH] gamma^(t+1)
@@ -183,19 +196,52 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
   const int tO = 2 * (tid / 16), jO = 4 * (tid % 16);    // O: rows tO..tO+1, cols jO..jO+3
   const int jS = 4 * (tid % 16);                          // S: rows i0..i0+7 (i0 = 8*(tid/16) + 128*r)
 
-  for (int c0 = lo; c0 < hi; c0 += CH) {
+  // async staging of rows [cc0, cc0 + CH): rows past the segment and columns past dv zero-fill
+  // (width: global row length; ldd: smem row stride; rowlen: staged columns, ncols of them valid)
+  auto stage_rows = [&](float* dst, const T* src, int cc0, int width, int ldd, int rowlen, int col0, int ncols) {
+    const int Lc = min(CH, hi - cc0);
+    const int per_row = rowlen / 4;
+    for (int e = tid; e < CH * per_row; e += NT) {
+      const int t = e / per_row, c4 = 4 * (e % per_row);
+      const bool ok = t < Lc && c4 < ncols;
+      const float* g = reinterpret_cast<const float*>(src) + (size_t)(cc0 + (ok ? t : 0)) * width + col0 + (ok ? c4 : 0);
+      cp_async16_zfill(dst + t * ldd + c4, g, ok ? 16 : 0);
+    }
+  };
+  if constexpr (ASYNC) {
+    if (lo < hi) {
+      if (!state_only) stage_rows(Qs, qb, lo, dk, ld, dk, 0, dk);
+      stage_rows(Ks, kb, lo, dk, ld, dk, 0, dk);
+      stage_rows(Vs, vb, lo, dv, DVT, DVT, j0, nj);
+    }
+    cp_async_commit_group();
+  }
+  int buf = 0;
+  for (int c0 = lo; c0 < hi; c0 += CH, buf ^= (NB - 1)) {
     const int L = min(CH, hi - c0);
     __syncthreads();
-    for (int e = tid; e < CH * dk; e += NT) {
-      const int t = e / dk, i = e % dk;
-      const bool in = t < L;
-      Ks[t * ld + i] = in ? to_f32(kb[(size_t)(c0 + t) * dk + i]) : 0.f;
-      if (!state_only) Qs[t * ld + i] = in ? to_f32(qb[(size_t)(c0 + t) * dk + i]) : 0.f;
+    if constexpr (ASYNC) {
+      // buffer buf^1 was last read by the previous chunk's state update (before the barrier)
+      if (c0 + CH < hi) {
+        stage_rows(Ks + (buf ^ 1) * CH * ld, kb, c0 + CH, dk, ld, dk, 0, dk);
+        stage_rows(Vs + (buf ^ 1) * CH * DVT, vb, c0 + CH, dv, DVT, DVT, j0, nj);
+      }
+      cp_async_commit_group();
+      cp_async_wait_one();               // this chunk's K, V (and Q) have landed for this thread
+    } else {
+      for (int e = tid; e < CH * dk; e += NT) {
+        const int t = e / dk, i = e % dk;
+        const bool in = t < L;
+        Ks[t * ld + i] = in ? to_f32(kb[(size_t)(c0 + t) * dk + i]) : 0.f;
+        if (!state_only) Qs[t * ld + i] = in ? to_f32(qb[(size_t)(c0 + t) * dk + i]) : 0.f;
+      }
+      for (int e = tid; e < CH * DVT; e += NT) {
+        const int t = e / DVT, j = e % DVT;
+        Vs[e] = (t < L && j < nj) ? to_f32(vb[(size_t)(c0 + t) * dv + j0 + j]) : 0.f;
+      }
     }
-    for (int e = tid; e < CH * DVT; e += NT) {
-      const int t = e / DVT, j = e % DVT;
-      Vs[e] = (t < L && j < nj) ? to_f32(vb[(size_t)(c0 + t) * dv + j0 + j]) : 0.f;
-    }
+    const float* Kc = Ks + buf * CH * ld;
+    const float* Vc = Vs + buf * CH * DVT;
     if (tid < CH) {
       w[tid] = tid < L ? gpow(lg, (float)(L - 1 - tid)) : 0.f;
       gq[tid] = gpow(lg, (float)(tid + 1));
@@ -209,7 +255,7 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
         if (sA <= tA + 1) {
           const float* q0 = Qs + tA * ld;
           const float* q1 = q0 + ld;
-          const float* k0 = Ks + sA * ld;
+          const float* k0 = Kc + sA * ld;
           const float* k1 = k0 + ld;
           for (int i = 0; i < dk; i += 4) {
             const float4 x0 = *reinterpret_cast<const float4*>(q0 + i);
@@ -237,7 +283,7 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
         float in0[4] = {0.f, 0.f, 0.f, 0.f}, in1[4] = {0.f, 0.f, 0.f, 0.f};
         float ex0[4] = {0.f, 0.f, 0.f, 0.f}, ex1[4] = {0.f, 0.f, 0.f, 0.f};
         for (int sc = 0; sc <= tO + 1 && sc < CH; ++sc) {
-          const float4 vv = *reinterpret_cast<const float4*>(Vs + sc * DVT + jO);
+          const float4 vv = *reinterpret_cast<const float4*>(Vc + sc * DVT + jO);
           const float a0 = A[tO * LA + sc], a1 = A[(tO + 1) * LA + sc];
           in0[0] = fmaf(a0, vv.x, in0[0]); in0[1] = fmaf(a0, vv.y, in0[1]);
           in0[2] = fmaf(a0, vv.z, in0[2]); in0[3] = fmaf(a0, vv.w, in0[3]);
@@ -267,6 +313,11 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
         }
       }
       __syncthreads();   // Q.S reads of S done before the update below
+      if constexpr (ASYNC) {
+        // every read of Q for this chunk is done: stream the next chunk's Q in behind the update
+        if (c0 + CH < hi) stage_rows(Qs, qb, c0 + CH, dk, ld, dk, 0, dk);
+        cp_async_commit_group();
+      }
     }
     // S <- gamma^L S + sum_s gamma^(L-1-s) k_s^T v_s   (rows i0..i0+7, columns jS..jS+3)
     const float carry = gpow(lg, (float)L);
@@ -278,9 +329,9 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
         for (int e = 0; e < 4; ++e) acc[r][e] = 0.f;
       for (int sc = 0; sc < L; ++sc) {
         const float ws = w[sc];
-        const float4 vv = *reinterpret_cast<const float4*>(Vs + sc * DVT + jS);
-        const float4 ka = *reinterpret_cast<const float4*>(Ks + sc * ld + i0);
-        const float4 kc = *reinterpret_cast<const float4*>(Ks + sc * ld + i0 + 4);
+        const float4 vv = *reinterpret_cast<const float4*>(Vc + sc * DVT + jS);
+        const float4 ka = *reinterpret_cast<const float4*>(Kc + sc * ld + i0);
+        const float4 kc = *reinterpret_cast<const float4*>(Kc + sc * ld + i0 + 4);
         const float kr[8] = {ws * ka.x, ws * ka.y, ws * ka.z, ws * ka.w, ws * kc.x, ws * kc.y, ws * kc.z, ws * kc.w};
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -322,18 +373,33 @@ cudaError_t launch_prefill_simt(const void* q, const void* k, const void* v, voi
   cudaError_t err;
   static const bool plain = getenv("LINATTN_SIMT_PLAIN") != nullptr;   // A/B switch
   if (s.dk % 8 == 0 && !plain) {
-    const size_t smem_rb = sizeof(float) * (2 * CH * ((size_t)s.dk + 4) + CH * DVT + CH * (CH + 4) +
-                                            (size_t)s.dk * DVT + 2 * CH);
+    static const bool sync_loads = getenv("LINATTN_SIMT_SYNC") != nullptr;   // A/B switch
+    const bool async = !sync_loads && dtype == LINATTN_F32 && s.dv % 4 == 0 &&
+                       !((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+                          reinterpret_cast<uintptr_t>(q)) & 15);
+    const size_t nb = async ? 2 : 1;
+    const size_t smem_rb = sizeof(float) * ((1 + nb) * CH * ((size_t)s.dk + 4) + nb * CH * DVT +
+                                            CH * (CH + 4) + (size_t)s.dk * DVT + 2 * CH);
+    if (async && smem_rb <= 227 * 1024) {
+      auto kern = prefill_simt_rb_kernel<float, true>;
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rb);
+      if (err != cudaSuccess) return err;
+      kern<<<grid, NT, smem_rb, stream>>>((const float*)q, (const float*)k, (const float*)v, (float*)o,
+                                          log2g, s_in, s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv,
+                                          state_only, sa);
+      count_launch();
+      return cudaGetLastError();
+    }
     if (smem_rb <= 227 * 1024) {
       if (dtype == LINATTN_BF16) {
-        auto kern = prefill_simt_rb_kernel<__nv_bfloat16>;
+        auto kern = prefill_simt_rb_kernel<__nv_bfloat16, false>;
         err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rb);
         if (err != cudaSuccess) return err;
         kern<<<grid, NT, smem_rb, stream>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                             (const __nv_bfloat16*)v, (__nv_bfloat16*)o, log2g, s_in, s_out,
                                             (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, state_only, sa);
       } else {
-        auto kern = prefill_simt_rb_kernel<float>;
+        auto kern = prefill_simt_rb_kernel<float, false>;
         err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rb);
         if (err != cudaSuccess) return err;
         kern<<<grid, NT, smem_rb, stream>>>((const float*)q, (const float*)k, (const float*)v, (float*)o,
