@@ -378,3 +378,49 @@ def test_recurrent_scan_kernel(la, dk, dv, dt):
         ops.recurrent(dev(b[:, :, :200], dt), dev(c[:, :, :200], dt), dev(v[:, :, :200], dt), l2, s_out=s_mid)
         tail = ops.recurrent(dev(b[:, :, 200:], dt), dev(c[:, :, 200:], dt), dev(v[:, :, 200:], dt), l2, s_in=s_mid)
         assert orc.max_rel_error(tail.float().cpu().numpy(), ref[:, :, 200:]) <= (TOL_F32 if dt == torch.float32 else TOL_BF16)
+
+
+def test_concurrent_threads_and_streams(la):
+    """Calls are pure and reentrant (reference SPEC.md:68): two host threads on their
+    own CUDA streams -- plain grid, balanced schedule and in-device split, plus a failing call --
+    give bitwise the results of the same calls made serially, and errors stay thread-local."""
+    import threading
+    from paper_2501_02573_b200 import ops
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    shapes = [(2, 3, 700, 128, 128), (1, sms + 3, 256, 64, 128), (1, 2, 4096, 128, 128)]
+    g = torch.Generator(device="cuda").manual_seed(3)
+    cases = []
+    for (B, H, N, dk, dv) in shapes:
+        q = torch.randn(B, H, N, dk, device="cuda", dtype=torch.bfloat16, generator=g)
+        k = torch.randn(B, H, N, dk, device="cuda", dtype=torch.bfloat16, generator=g)
+        v = torch.randn(B, H, N, dv, device="cuda", dtype=torch.bfloat16, generator=g)
+        l2 = ops.log2_gamma([0.9 + 0.09 * (h % 2) for h in range(H)], True, "cuda")
+        cases.append((q, k, v, l2))
+    serial = [ops.prefill(*c) for c in cases]
+    torch.cuda.synchronize()
+    results, errors = {}, []
+
+    def worker(tid):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(3):
+                    for i, c in enumerate(cases):
+                        results[(tid, rep, i)] = ops.prefill(*c)
+                if tid == 1:   # a failing C call on this thread: thread-local status and message
+                    from paper_2501_02573_b200 import _lib
+                    lib = _lib.load()
+                    with pytest.raises(la.ShapeError, match="seqlen"):
+                        _lib.check(lib.linattn_prefill(1, 1, 1, 1, 1, None, None, 1, 1, 0, 4, 4, 1, 0, None))
+            s.synchronize()
+        except Exception as e:   # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for (tid, rep, i), out in results.items():
+        assert torch.equal(out, serial[i]), (tid, rep, i)
