@@ -282,23 +282,33 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
       {
         float in0[4] = {0.f, 0.f, 0.f, 0.f}, in1[4] = {0.f, 0.f, 0.f, 0.f};
         float ex0[4] = {0.f, 0.f, 0.f, 0.f}, ex1[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int sc = 0; sc <= tO + 1 && sc < CH; ++sc) {
-          const float4 vv = *reinterpret_cast<const float4*>(Vc + sc * DVT + jO);
-          const float a0 = A[tO * LA + sc], a1 = A[(tO + 1) * LA + sc];
-          in0[0] = fmaf(a0, vv.x, in0[0]); in0[1] = fmaf(a0, vv.y, in0[1]);
-          in0[2] = fmaf(a0, vv.z, in0[2]); in0[3] = fmaf(a0, vv.w, in0[3]);
-          in1[0] = fmaf(a1, vv.x, in1[0]); in1[1] = fmaf(a1, vv.y, in1[1]);
-          in1[2] = fmaf(a1, vv.z, in1[2]); in1[3] = fmaf(a1, vv.w, in1[3]);
+        // four reduction steps per iteration: one float4 of A (or Q) per row feeds 16 FMAs
+        // (A is zero above the diagonal, so the intra loop runs to the next multiple of 4)
+        auto step4 = [](float (&acc)[4], const float4 a, const float4& b0, const float4& b1,
+                        const float4& b2, const float4& b3) {
+          acc[0] = fmaf(a.x, b0.x, fmaf(a.y, b1.x, fmaf(a.z, b2.x, fmaf(a.w, b3.x, acc[0]))));
+          acc[1] = fmaf(a.x, b0.y, fmaf(a.y, b1.y, fmaf(a.z, b2.y, fmaf(a.w, b3.y, acc[1]))));
+          acc[2] = fmaf(a.x, b0.z, fmaf(a.y, b1.z, fmaf(a.z, b2.z, fmaf(a.w, b3.z, acc[2]))));
+          acc[3] = fmaf(a.x, b0.w, fmaf(a.y, b1.w, fmaf(a.z, b2.w, fmaf(a.w, b3.w, acc[3]))));
+        };
+        const int sc_end = min(CH, (tO + 2 + 3) & ~3);
+        for (int sc = 0; sc < sc_end; sc += 4) {
+          const float4 v0 = *reinterpret_cast<const float4*>(Vc + (sc + 0) * DVT + jO);
+          const float4 v1 = *reinterpret_cast<const float4*>(Vc + (sc + 1) * DVT + jO);
+          const float4 v2 = *reinterpret_cast<const float4*>(Vc + (sc + 2) * DVT + jO);
+          const float4 v3 = *reinterpret_cast<const float4*>(Vc + (sc + 3) * DVT + jO);
+          step4(in0, *reinterpret_cast<const float4*>(A + tO * LA + sc), v0, v1, v2, v3);
+          step4(in1, *reinterpret_cast<const float4*>(A + (tO + 1) * LA + sc), v0, v1, v2, v3);
         }
         const float* q0 = Qs + tO * ld;
         const float* q1 = q0 + ld;
-        for (int i = 0; i < dk; ++i) {
-          const float4 sv = *reinterpret_cast<const float4*>(S + i * DVT + jO);
-          const float x0 = q0[i], x1 = q1[i];
-          ex0[0] = fmaf(x0, sv.x, ex0[0]); ex0[1] = fmaf(x0, sv.y, ex0[1]);
-          ex0[2] = fmaf(x0, sv.z, ex0[2]); ex0[3] = fmaf(x0, sv.w, ex0[3]);
-          ex1[0] = fmaf(x1, sv.x, ex1[0]); ex1[1] = fmaf(x1, sv.y, ex1[1]);
-          ex1[2] = fmaf(x1, sv.z, ex1[2]); ex1[3] = fmaf(x1, sv.w, ex1[3]);
+        for (int i = 0; i < dk; i += 4) {
+          const float4 s0 = *reinterpret_cast<const float4*>(S + (i + 0) * DVT + jO);
+          const float4 s1 = *reinterpret_cast<const float4*>(S + (i + 1) * DVT + jO);
+          const float4 s2 = *reinterpret_cast<const float4*>(S + (i + 2) * DVT + jO);
+          const float4 s3 = *reinterpret_cast<const float4*>(S + (i + 3) * DVT + jO);
+          step4(ex0, *reinterpret_cast<const float4*>(q0 + i), s0, s1, s2, s3);
+          step4(ex1, *reinterpret_cast<const float4*>(q1 + i), s0, s1, s2, s3);
         }
 #pragma unroll
         for (int dt = 0; dt < 2; ++dt) {
