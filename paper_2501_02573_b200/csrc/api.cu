@@ -233,6 +233,22 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
     }
     cudaGetLastError();
   }
+  // FFMA kernel (compute-bound, two or more CTAs per SM): the same schedule over the resident
+  // slots whenever the units are not a whole number of waves
+  if (!tc && balance_env != 0) {
+    const int slots = simt_balance_slots(q, k, v, s, dtype);
+    const int64_t su = s.B * s.H * ceil_div(s.dv, 64);
+    if (slots > 0 && su > slots && su % slots != 0) {
+      void* ws = nullptr;
+      cudaMemPool_t pool = work_pool();
+      if (pool && cudaMallocFromPoolAsync(&ws, simt_balance_workspace_bytes(s, slots), pool, st) == cudaSuccess) {
+        cudaError_t e = launch_prefill_simt_balanced(q, k, v, o, log2g, s_in, s_out, s, dtype, slots, ws, st);
+        cudaFreeAsync(ws, st);
+        if (e != cudaErrorNotSupported) return cuda_status(e, "prefill_simt (balanced)");
+      }
+      cudaGetLastError();
+    }
+  }
   return cuda_status(launch(q, o, s_in, s_out, false, SegArgs{}, 1), what);
 }
 

@@ -89,7 +89,8 @@ __device__ __forceinline__ float seg_loc_weight(const SegArgs& sa, int q, int N,
 struct Balance {
   int on = 0;
   int units = 0, nc = 0, w = 0, ntiles = 1;
-  float* hst = nullptr;          // [grid][dk][128] fp32 hand-off states
+  int chunk = 64, tile = 128;    // tokens per chunk, dv columns per unit
+  float* hst = nullptr;          // [grid][dk][tile] fp32 hand-off states
   unsigned* flags = nullptr;     // [grid] published flags, then the ticket counter (zeroed per launch)
 };
 
@@ -120,7 +121,7 @@ __device__ __forceinline__ WorkItem balance_item(const Balance& P, int N, int t,
   if (ce != 0 && k == 0) {                    // head of unit ue: publish its end state
     u = ue;
     w.lo = 0;
-    w.hi = ce * 64;
+    w.hi = ce * P.chunk;
     w.out_slot = t;
   } else {
     const int kk = k - (ce != 0);
@@ -130,13 +131,13 @@ __device__ __forceinline__ WorkItem balance_item(const Balance& P, int N, int t,
       w.hi = N;
     } else {                                  // tail of unit us, seeded by the previous range's head
       u = us;
-      w.lo = cs * 64;
+      w.lo = cs * P.chunk;
       w.hi = N;
       w.in_slot = t - 1;
     }
   }
   w.bh = u / P.ntiles;
-  w.j0 = (u % P.ntiles) * 128;
+  w.j0 = (u % P.ntiles) * P.tile;
   return w;
 }
 
@@ -146,6 +147,15 @@ cudaError_t launch_prefill_simt(const void* q, const void* k, const void* v, voi
                                 const float* log2g, const float* s_in, float* s_out,
                                 const ShapeArgs& s, int dtype, bool state_only,
                                 const SegArgs& sa, int nz, cudaStream_t stream);
+
+// Balanced persistent FFMA prefill (chunk 32, 64-wide dv tiles): slots = resident CTAs on the
+// device for this shape (0 = not applicable); `ws` holds simt_balance_workspace_bytes bytes.
+int simt_balance_slots(const void* q, const void* k, const void* v, const ShapeArgs& s, int dtype);
+size_t simt_balance_workspace_bytes(const ShapeArgs& s, int slots);
+cudaError_t launch_prefill_simt_balanced(const void* q, const void* k, const void* v, void* o,
+                                         const float* log2g, const float* s_in, float* s_out,
+                                         const ShapeArgs& s, int dtype, int slots, void* ws,
+                                         cudaStream_t stream);
 
 // Returns cudaErrorNotSupported when the shape is outside the TC kernel's envelope.
 cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void* o,

@@ -139,15 +139,25 @@ __device__ __forceinline__ void cp_async16_zfill(float* dst, const float* src, i
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src), "r"(src_bytes) : "memory");
 }
+__device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-template <typename T, bool ASYNC>
+// BAL: balanced persistent schedule (Balance mode 0, chunk CH, tile DVT): one CTA per resident
+// slot walks its work list (head -> published hand-off state, whole units, seeded tail).
+template <typename T, bool ASYNC, bool BAL>
 __global__ void __launch_bounds__(NT)
 prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
                        T* __restrict__ o, const float* __restrict__ log2g,
                        const float* __restrict__ s_in, float* __restrict__ s_out,
-                       int H, int N, int dk, int dv, int state_only, const SegArgs sa) {
+                       int H, int N, int dk, int dv, int state_only, const SegArgs sa, const Balance bal) {
   static_assert(!ASYNC || sizeof(T) == 4, "cp.async staging copies fp32 rows");
   extern __shared__ __align__(16) float smem[];
   const int ld = dk + 4;                      // 16-byte rows, bank-spread
@@ -161,21 +171,52 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
   float* gq = w + CH;                         // [CH] gamma^(t+1)
   constexpr int LA = CH + 4;
 
-  const int bh = blockIdx.y;
-  const int h = bh % H;
-  const int j0 = blockIdx.x * DVT;
-  const int nj = min(DVT, dv - j0);
   const int tid = threadIdx.x;
-  const float lg = log2g[h];
-  int lo, hi;
-  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
   const size_t per_state = (size_t)gridDim.y * dk * dv;
+  // thread tiles
+  const int tA = 2 * (tid / 16), sA = 2 * (tid % 16);    // A: rows tA..tA+1, cols sA..sA+1
+  const int tO = 2 * (tid / 16), jO = 4 * (tid % 16);    // O: rows tO..tO+1, cols jO..jO+3
+  const int jS = 4 * (tid % 16);                          // S: rows i0..i0+7 (i0 = 8*(tid/16) + 128*r)
+
+  __shared__ int s_ticket;
+  int ticket = 0, nitems = 1;
+  long long r0 = 0, r1 = 0;
+  if constexpr (BAL) {
+    if (tid == 0) s_ticket = (int)atomicAdd(bal.flags + gridDim.x, 1u);   // start order
+    __syncthreads();
+    ticket = s_ticket;
+    nitems = balance_items(bal, ticket, r0, r1);
+  }
+  for (int it = 0; it < nitems; ++it) {
+  WorkItem wi;
+  if constexpr (BAL) {
+    wi = balance_item(bal, N, ticket, it, r0, r1);
+  } else {
+    wi.bh = blockIdx.y;
+    wi.j0 = blockIdx.x * DVT;
+    seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, wi.lo, wi.hi);
+    wi.in_slot = wi.out_slot = -1;
+  }
+  const int bh = wi.bh;
+  const int h = bh % H;
+  const int j0 = wi.j0;
+  const int nj = min(DVT, dv - j0);
+  const int lo = wi.lo, hi = wi.hi;
+  const float lg = log2g[h];
   const T* qb = q + (size_t)bh * N * dk;
   const T* kb = k + (size_t)bh * N * dk;
   const T* vb = v + (size_t)bh * N * dv;
   T* ob = o ? o + (size_t)bh * N * dv : nullptr;
 
-  {
+  if (BAL && it > 0) __syncthreads();        // the previous item's end-state reads of S are done
+  if (BAL && wi.in_slot >= 0) {
+    // balanced tail: the previous range's head published the state at lo (s_in included)
+    if (tid == 0)
+      while (ld_acquire_gpu_u32(bal.flags + wi.in_slot) == 0u) __nanosleep(256);
+    __syncthreads();
+    const float* hp = bal.hst + (size_t)wi.in_slot * dk * DVT;
+    for (int e = tid; e < dk * DVT; e += NT) S[e] = (e % DVT) < nj ? __ldcg(hp + e) : 0.f;
+  } else {
     const float w_in = gpow(lg, (float)lo);
     for (int e = tid; e < dk * DVT; e += NT) {
       const int i = e / DVT, j = e % DVT;
@@ -191,10 +232,6 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
       }
     }
   }
-  // thread tiles
-  const int tA = 2 * (tid / 16), sA = 2 * (tid % 16);    // A: rows tA..tA+1, cols sA..sA+1
-  const int tO = 2 * (tid / 16), jO = 4 * (tid % 16);    // O: rows tO..tO+1, cols jO..jO+3
-  const int jS = 4 * (tid % 16);                          // S: rows i0..i0+7 (i0 = 8*(tid/16) + 128*r)
 
   // async staging of rows [cc0, cc0 + CH): rows past the segment and columns past dv zero-fill
   // (width: global row length; ldd: smem row stride; rowlen: staged columns, ncols of them valid)
@@ -364,13 +401,61 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
     }
   }
   __syncthreads();
-  if (s_out && (state_only || blockIdx.z == gridDim.z - 1)) {
+  if (BAL && wi.out_slot >= 0) {
+    // balanced head: publish the end state to the next range's tail
+    float* hp = bal.hst + (size_t)wi.out_slot * dk * DVT;
+    for (int e = tid; e < dk * DVT; e += NT) hp[e] = S[e];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release_gpu_u32(bal.flags + wi.out_slot, 1u);
+  } else if (s_out && (BAL ? hi == N : (state_only || blockIdx.z == gridDim.z - 1))) {
     float* so = s_out + (state_only ? blockIdx.z * per_state : 0);
     for (int e = tid; e < dk * DVT; e += NT) {
       const int i = e / DVT, j = e % DVT;
       if (j < nj) so[((size_t)bh * dk + i) * dv + j0 + j] = S[e];
     }
   }
+  }  // work items
+}
+
+}  // namespace
+
+namespace {
+
+// Register-blocked variant selection: 0 = none (plain kernel), 1 = synchronous loads, 2 = cp.async.
+int rb_mode(const void* q, const void* k, const void* v, const ShapeArgs& s, int dtype, size_t& smem) {
+  static const bool plain = getenv("LINATTN_SIMT_PLAIN") != nullptr;       // A/B switch
+  static const bool sync_loads = getenv("LINATTN_SIMT_SYNC") != nullptr;   // A/B switch
+  if (s.dk % 8 != 0 || plain) return 0;
+  const bool async = !sync_loads && dtype == LINATTN_F32 && s.dv % 4 == 0 &&
+                     !((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+                        reinterpret_cast<uintptr_t>(q)) & 15);
+  for (int nb = async ? 2 : 1; nb >= 1; --nb) {
+    smem = sizeof(float) * ((1 + nb) * CH * ((size_t)s.dk + 4) + nb * CH * DVT + CH * (CH + 4) +
+                            (size_t)s.dk * DVT + 2 * CH);
+    if (smem <= 227 * 1024) return nb == 2 ? 2 : 1;
+  }
+  return 0;
+}
+
+template <bool BAL>
+cudaError_t launch_rb(int mode, const void* q, const void* k, const void* v, void* o, const float* log2g,
+                      const float* s_in, float* s_out, const ShapeArgs& s, int dtype, bool state_only,
+                      const SegArgs& sa, const Balance& bal, dim3 grid, size_t smem, cudaStream_t stream) {
+  auto go = [&](auto kern, auto tp) -> cudaError_t {
+    using TT = typename decltype(tp)::type;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    kern<<<grid, NT, smem, stream>>>((const TT*)q, (const TT*)k, (const TT*)v, (TT*)o, log2g, s_in, s_out,
+                                     (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, state_only ? 1 : 0, sa, bal);
+    count_launch();
+    return cudaGetLastError();
+  };
+  struct F { using type = float; };
+  struct Hb { using type = __nv_bfloat16; };
+  if (mode == 2) return go(prefill_simt_rb_kernel<float, true, BAL>, F{});
+  if (dtype == LINATTN_BF16) return go(prefill_simt_rb_kernel<__nv_bfloat16, false, BAL>, Hb{});
+  return go(prefill_simt_rb_kernel<float, false, BAL>, F{});
 }
 
 }  // namespace
@@ -381,45 +466,10 @@ cudaError_t launch_prefill_simt(const void* q, const void* k, const void* v, voi
                                 const SegArgs& sa, int nz, cudaStream_t stream) {
   dim3 grid((unsigned)((s.dv + DVT - 1) / DVT), (unsigned)(s.B * s.H), (unsigned)nz);
   cudaError_t err;
-  static const bool plain = getenv("LINATTN_SIMT_PLAIN") != nullptr;   // A/B switch
-  if (s.dk % 8 == 0 && !plain) {
-    static const bool sync_loads = getenv("LINATTN_SIMT_SYNC") != nullptr;   // A/B switch
-    const bool async = !sync_loads && dtype == LINATTN_F32 && s.dv % 4 == 0 &&
-                       !((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
-                          reinterpret_cast<uintptr_t>(q)) & 15);
-    const size_t nb = async ? 2 : 1;
-    const size_t smem_rb = sizeof(float) * ((1 + nb) * CH * ((size_t)s.dk + 4) + nb * CH * DVT +
-                                            CH * (CH + 4) + (size_t)s.dk * DVT + 2 * CH);
-    if (async && smem_rb <= 227 * 1024) {
-      auto kern = prefill_simt_rb_kernel<float, true>;
-      err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rb);
-      if (err != cudaSuccess) return err;
-      kern<<<grid, NT, smem_rb, stream>>>((const float*)q, (const float*)k, (const float*)v, (float*)o,
-                                          log2g, s_in, s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv,
-                                          state_only, sa);
-      count_launch();
-      return cudaGetLastError();
-    }
-    if (smem_rb <= 227 * 1024) {
-      if (dtype == LINATTN_BF16) {
-        auto kern = prefill_simt_rb_kernel<__nv_bfloat16, false>;
-        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rb);
-        if (err != cudaSuccess) return err;
-        kern<<<grid, NT, smem_rb, stream>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
-                                            (const __nv_bfloat16*)v, (__nv_bfloat16*)o, log2g, s_in, s_out,
-                                            (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, state_only, sa);
-      } else {
-        auto kern = prefill_simt_rb_kernel<float, false>;
-        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rb);
-        if (err != cudaSuccess) return err;
-        kern<<<grid, NT, smem_rb, stream>>>((const float*)q, (const float*)k, (const float*)v, (float*)o,
-                                            log2g, s_in, s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv,
-                                            state_only, sa);
-      }
-      count_launch();
-      return cudaGetLastError();
-    }
-  }
+  size_t smem_rb = 0;
+  if (const int mode = rb_mode(q, k, v, s, dtype, smem_rb))
+    return launch_rb<false>(mode, q, k, v, o, log2g, s_in, s_out, s, dtype, state_only, sa, Balance{}, grid,
+                            smem_rb, stream);
   const size_t ldq = (size_t)s.dk + 1;
   const size_t smem = sizeof(float) * (2 * CH * ldq + CH * DVT + CH * (CH + 1) +
                                        (size_t)s.dk * DVT + CH);
@@ -441,6 +491,60 @@ cudaError_t launch_prefill_simt(const void* q, const void* k, const void* v, voi
   }
   count_launch();
   return cudaGetLastError();
+}
+
+int simt_balance_slots(const void* q, const void* k, const void* v, const ShapeArgs& s, int dtype) {
+  size_t smem = 0;
+  const int mode = rb_mode(q, k, v, s, dtype, smem);
+  if (mode == 0) return 0;
+  auto kern = mode == 2 ? prefill_simt_rb_kernel<float, true, true>
+                        : (dtype == LINATTN_BF16 ? nullptr : prefill_simt_rb_kernel<float, false, true>);
+  int per_sm = 0, dev = 0, sms = 0;
+  if (kern) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) != cudaSuccess)
+      return 0;
+  } else {
+    auto kb = prefill_simt_rb_kernel<__nv_bfloat16, false, true>;
+    if (cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, NT, smem) != cudaSuccess)
+      return 0;
+  }
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return per_sm * sms;
+}
+
+size_t simt_balance_workspace_bytes(const ShapeArgs& s, int slots) {
+  return 256 * (size_t)((slots + 1 + 63) / 64) + (size_t)slots * s.dk * DVT * sizeof(float);
+}
+
+cudaError_t launch_prefill_simt_balanced(const void* q, const void* k, const void* v, void* o,
+                                         const float* log2g, const float* s_in, float* s_out,
+                                         const ShapeArgs& s, int dtype, int slots, void* ws,
+                                         cudaStream_t stream) {
+  size_t smem = 0;
+  const int mode = rb_mode(q, k, v, s, dtype, smem);
+  const int64_t ntiles = (s.dv + DVT - 1) / DVT;
+  const int64_t units = s.B * s.H * ntiles, nc = (s.N + CH - 1) / CH;
+  const int64_t w = (units * nc + slots - 1) / slots;
+  if (mode == 0 || w < nc || units * nc > (1LL << 31) - 1) return cudaErrorNotSupported;
+  Balance bal;
+  bal.on = 1;
+  bal.units = (int)units;
+  bal.nc = (int)nc;
+  bal.w = (int)w;
+  bal.ntiles = (int)ntiles;
+  bal.chunk = CH;
+  bal.tile = DVT;
+  bal.flags = static_cast<unsigned*>(ws);
+  bal.hst = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256 * (size_t)((slots + 1 + 63) / 64));
+  const int used = (int)((units * nc + w - 1) / w);
+  cudaError_t err = cudaMemsetAsync(ws, 0, sizeof(unsigned) * (slots + 1), stream);
+  if (err != cudaSuccess) return err;
+  return launch_rb<true>(mode, q, k, v, o, log2g, s_in, s_out, s, dtype, false, SegArgs{}, bal, dim3(used), smem,
+                         stream);
 }
 
 }  // namespace linattn

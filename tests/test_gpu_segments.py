@@ -230,3 +230,18 @@ def test_balanced_schedule(ops, B, H, dk, dv, N):
     # repeated launches reuse the pooled workspace (flags re-zeroed per launch)
     again = ops.prefill(q, k, vv, l2, s_in=dev(s0))
     assert torch.equal(again, out)
+
+
+@pytest.mark.parametrize("B,H,N,dk,dv", [(3, 53, 300, 128, 128), (2, 80, 1000, 64, 96), (1, 150, 65, 32, 64)])
+def test_balanced_schedule_fp32(ops, B, H, N, dk, dv):
+    """The FFMA kernel's balanced persistent schedule (more 64-wide units than resident CTAs):
+    fp32 parity with s_in seeding and s_out at the 1e-4 bar."""
+    gam = [0.0, 1.0] + [1 - 2.0 ** (-3 - (h % 12)) for h in range(H - 2)]
+    b, c, v = orc.gen_inputs(B, H, N, dk, dv, np.float32, 60 + N)
+    s0 = np.random.default_rng(N).standard_normal((B, H, dk, dv)).astype(np.float32) * 0.05
+    ref, ref_s = orc.seeded_blocked_attn(b, c, v, gam, True, s0.astype(np.float64), block=64)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    s_out = torch.full((B, H, dk, dv), float("nan"), device="cuda")
+    out = ops.prefill(dev(b), dev(c), dev(v), l2, s_in=dev(s0), s_out=s_out, kernel="simt")
+    assert orc.max_rel_error(out.cpu().numpy(), ref) <= TOL_F32
+    assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= TOL_F32
