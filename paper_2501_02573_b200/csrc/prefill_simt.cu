@@ -493,23 +493,25 @@ cudaError_t launch_prefill_simt(const void* q, const void* k, const void* v, voi
   return cudaGetLastError();
 }
 
+namespace {
+template <typename K>
+int resident_per_sm(K kern, size_t smem) {
+  int n = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, NT, smem) != cudaSuccess)
+    return 0;
+  return n;
+}
+}  // namespace
+
 int simt_balance_slots(const void* q, const void* k, const void* v, const ShapeArgs& s, int dtype) {
   size_t smem = 0;
   const int mode = rb_mode(q, k, v, s, dtype, smem);
   if (mode == 0) return 0;
-  auto kern = mode == 2 ? prefill_simt_rb_kernel<float, true, true>
-                        : (dtype == LINATTN_BF16 ? nullptr : prefill_simt_rb_kernel<float, false, true>);
-  int per_sm = 0, dev = 0, sms = 0;
-  if (kern) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) != cudaSuccess)
-      return 0;
-  } else {
-    auto kb = prefill_simt_rb_kernel<__nv_bfloat16, false, true>;
-    if (cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, NT, smem) != cudaSuccess)
-      return 0;
-  }
+  const int per_sm = mode == 2 ? resident_per_sm(prefill_simt_rb_kernel<float, true, true>, smem)
+                     : dtype == LINATTN_BF16 ? resident_per_sm(prefill_simt_rb_kernel<__nv_bfloat16, false, true>, smem)
+                                             : resident_per_sm(prefill_simt_rb_kernel<float, false, true>, smem);
+  int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return 0;
