@@ -424,3 +424,36 @@ def test_concurrent_threads_and_streams(la):
     assert not errors, errors
     for (tid, rep, i), out in results.items():
         assert torch.equal(out, serial[i]), (tid, rep, i)
+
+
+def _sampled_slices_match(o, q, k, v, gam, picks, tol=TOL_BF16):
+    """Sampled (b, h) slices of a full-size output against the seeded f64 blocked oracle."""
+    for (bi, h) in picks:
+        sl = lambda t: t[bi:bi + 1, h:h + 1].float().cpu().numpy()   # noqa: E731
+        ref, _ = orc.seeded_blocked_attn(sl(q), sl(k), sl(v), [gam[h]], True, None, block=64)
+        assert orc.max_rel_error(o[bi, h].float().cpu().numpy(), ref[0, 0]) <= tol, (bi, h)
+
+
+def test_full_size_configs2_configs4_and_balanced(la):
+    """Full BASELINE.json sizes the dense oracle cannot take: configs[2] (dk=256/dv=512 clusters),
+    configs[4] (N=131072, in-device split) and a 160-unit balanced launch, on sampled slices of
+    the f64 blocked oracle; plus the split/no-split agreement and the end state at configs[4]."""
+    from paper_2501_02573_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(11)
+    for (B, H, N, dk, dv, picks) in [(4, 16, 16384, 256, 512, [(0, 0), (3, 15)]),
+                                     (1, 32, 131072, 128, 128, [(0, 0), (0, 31)]),
+                                     (5, 32, 8192, 128, 128, [(0, 0), (2, 7), (4, 31)])]:
+        q = torch.randn(B, H, N, dk, device="cuda", dtype=torch.bfloat16, generator=g)
+        k = torch.randn(B, H, N, dk, device="cuda", dtype=torch.bfloat16, generator=g)
+        v = torch.randn(B, H, N, dv, device="cuda", dtype=torch.bfloat16, generator=g)
+        gam = [1 - 2.0 ** (-5 - 10 * h / (H - 1)) for h in range(H)]
+        l2 = ops.log2_gamma(gam, True, "cuda")
+        s_out = torch.empty(B, H, dk, dv, device="cuda")
+        o = ops.prefill(q, k, v, l2, s_out=s_out)
+        _sampled_slices_match(o, q, k, v, gam, picks)
+        if N == 131072:
+            one = ops.prefill(q, k, v, l2, seq_split=1)     # single pass, no split
+            assert orc.max_rel_error(o.float().cpu().numpy(), one.float().cpu().numpy()) <= TOL_BF16
+            ref_s = orc.segment_end_state(k[0, 31].float().cpu().numpy(), v[0, 31].float().cpu().numpy(), gam[31])
+            assert orc.max_rel_error(s_out[0, 31].cpu().numpy(), ref_s) <= 5e-3
+        del q, k, v, o
