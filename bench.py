@@ -290,6 +290,31 @@ def bench_cfg3(args, ops, dev, g, hbm, tc_burst, barrier, max_over_ranks):
             "kernel": "prefill_tc (dk=256: state in TMEM)"}
 
 
+def bench_fp32(args, ops, dev, g, hbm, barrier, max_over_ranks):
+    """configs[1] shape in fp32 -- the reference's own arithmetic type: the fp32 parity mode
+    (FFMA kernel, <= 1e-4 vs the f64 oracle), the default route for fp32 inputs."""
+    import torch
+    B, H, N, d = 8, 32, 8192, 128
+    q = torch.randn(B, H, N, d, device=dev, dtype=torch.float32, generator=g)
+    k = torch.randn(B, H, N, d, device=dev, dtype=torch.float32, generator=g)
+    v = torch.randn(B, H, N, d, device=dev, dtype=torch.float32, generator=g)
+    out = torch.empty_like(v)
+    l2 = ops.log2_gamma(gammas(H), True, dev)
+    ms = _time_events(lambda: ops.prefill(q, k, v, l2, out=out, kernel="simt"), 5, barrier, max_over_ranks)
+    # FFMA work the kernel issues per (token, head) at chunk 32 and 64-wide dv tiles (two tiles):
+    # Q.K over the causal half of each chunk, A.V, Q.S, and the K^T V state update
+    fma = B * H * N * (2 * (17 * d) + 2 * (17 * 64) + 2 * (d * 64) + 2 * (d * 64))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = sms * 128 * 2 * 1.965e9 / 1e12          # FP32 FFMA TFLOP/s at the 1965 MHz max clock
+    tf = 2 * fma / (ms * 1e-3) / 1e12
+    del q, k, v, out
+    return {"workload": "configs[1] shape B=8,H=32,N=8192,d=128 in fp32 (b200-chunked-f32)",
+            "ms_per_step": ms, "tokens_per_s": B * N / (ms * 1e-3),
+            "hbm_gbs": B * H * N * 4 * 4 * d / (ms * 1e-3) / 1e9,
+            "ffma_tflops_issued": tf, "ffma_frac_of_peak": tf / peak, "ffma_peak_tflops": peak,
+            "kernel": "prefill_simt (fp32 FFMA, cp.async staging, balanced schedule)"}
+
+
 def bench_seqpar(args, ops, dev, g, hbm, world, rank, barrier, max_over_ranks):
     """configs[4]: B=1, H=32, N=131072, d=128 -- one job; N>1: sequence parallel over ranks."""
     import torch
@@ -419,6 +444,7 @@ def run_ours(args):
     # split inside the GPU at N=1, sequence parallel over the ranks (one NCCL all-gather) at N>1
     cfg3 = None if args.no_extra else bench_cfg3(args, ops, dev, g, hbm, tc_burst, barrier, max_over_ranks)
     cfg5 = None if args.no_extra else bench_seqpar(args, ops, dev, g, hbm, world, rank, barrier, max_over_ranks)
+    f32 = None if args.no_extra else bench_fp32(args, ops, dev, g, hbm, barrier, max_over_ranks)
 
     # CPU baseline (oracle port of the reference's CPU blocking route), rank 0 at N=1 only
     cpu = None
@@ -464,6 +490,7 @@ def run_ours(args):
         "decode": dec,
         "prefill_configs2": cfg3,
         "seqpar_configs4": cfg5,
+        "prefill_fp32_configs1": f32,
         "cpu_baseline": cpu,
     }
     if rank == 0:
