@@ -1184,6 +1184,46 @@ cudaError_t launch_tmem_state_mc(const CUtensorMap& mq, const CUtensorMap& mk, c
   return cudaGetLastError();
 }
 
+// Co-resident clusters of the dk=256 kernel for cluster size m on the current device (cached).
+template <int DK, int STAGES>
+int max_active_clusters(int m) {
+  static std::mutex mu;
+  static int cache[64][5] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || m < 1 || m > 4) return 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache[dev][m] != 0) return cache[dev][m];
+  using G = v3::Cfg<DK, STAGES>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(4 * m));
+  cfg.blockDim = dim3(v3::kThreads);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = m;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  cudaError_t err = cudaErrorInvalidValue;
+  if (m == 4) {
+    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 4>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) == cudaSuccess)
+      err = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+  } else if (m == 2) {
+    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 2>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) == cudaSuccess)
+      err = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+  }
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cache[dev][m] = n;
+  return n;
+}
+
 template <int DK, int STAGES>
 cudaError_t launch_tmem_state(const void* q, const void* k, const void* v, void* o, const float* log2g,
                               const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
@@ -1198,12 +1238,30 @@ cudaError_t launch_tmem_state(const void* q, const void* k, const void* v, void*
   }
   CUtensorMap mo = mk;
   if (!state_only && !make_map(&mo, o, s.dv, s.N, BH)) return cudaErrorInvalidValue;
-  // the dv tiles of a head share every Q/K tile: cluster them and multicast (LINATTN_NO_MULTICAST=1: off)
+  // the dv tiles of a head share every Q/K tile: cluster them and multicast (LINATTN_NO_MULTICAST=1: off).
+  // Cluster size = the one with the fewest waves of co-resident clusters (ties: the larger one):
+  // GPC packing fits only 32 four-CTA clusters (128 SMs) but 74 two-CTA ones (all 148), so e.g.
+  // 36 heads x 4 tiles run in one wave of pairs instead of two waves of quads.
   const int64_t tiles = (s.dv + kDVT - 1) / kDVT;
+  const int64_t ctas = tiles * s.B * s.H * nz;
   static const bool no_mc = getenv("LINATTN_NO_MULTICAST") != nullptr;
-  if (!no_mc && tiles == 4)
+  int mc = 1;
+  if (!no_mc) {
+    int64_t best = -1;
+    for (int m : {4, 2}) {
+      if (tiles % m != 0) continue;
+      const int slots = max_active_clusters<DK, STAGES>(m);
+      if (slots <= 0) continue;
+      const int64_t waves = (ctas / m + slots - 1) / slots;
+      if (best < 0 || waves < best) {
+        best = waves;
+        mc = m;
+      }
+    }
+  }
+  if (mc == 4)
     return launch_tmem_state_mc<DK, STAGES, 4>(mq, mk, mv, mo, log2g, s_in, s_out, s, state_only, sa, nz, stream);
-  if (!no_mc && tiles == 2)
+  if (mc == 2)
     return launch_tmem_state_mc<DK, STAGES, 2>(mq, mk, mv, mo, log2g, s_in, s_out, s, state_only, sa, nz, stream);
   return launch_tmem_state_mc<DK, STAGES, 1>(mq, mk, mv, mo, log2g, s_in, s_out, s, state_only, sa, nz, stream);
 }
