@@ -1,3 +1,4 @@
+"""Dev driver for ncu: the fp32 FFMA prefill at B=8,H=32,N=2048,d=128, twice."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

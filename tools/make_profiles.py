@@ -21,6 +21,8 @@ CAPTURES = [
     ("cfg5_statepass", "state_pass_split", 32 * 98304 * 512, "configs[4] phase A: K,V of segments 0..2 (98304 tokens x 32 heads)"),
     ("cfg5_prefill", "prefill_split", 32 * 131072 * 1024, "configs[4] phase B: 4 seeded segments x 32 heads"),
     ("decode", "decode_step", 256 * 32 * 132096, "configs[3] decode step B=256,H=32,d=128"),
+    ("fp32_prefill", "prefill_simt_fp32", 8 * 32 * 2048 * 2048,
+     "fp32 parity mode (FFMA) B=8,H=32,N=2048,d=128 (tools/f32_once.py): balanced, cp.async staging"),
 ]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
