@@ -457,3 +457,30 @@ def test_full_size_configs2_configs4_and_balanced(la):
             ref_s = orc.segment_end_state(k[0, 31].float().cpu().numpy(), v[0, 31].float().cpu().numpy(), gam[31])
             assert orc.max_rel_error(s_out[0, 31].cpu().numpy(), ref_s) <= 5e-3
         del q, k, v, o
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_random_shapes_fuzz(la, seed):
+    """Seeded random shapes across every dispatch branch (tensor cores dk in {64,128,256}, FFMA any
+    dk/dv, sequence split, balanced schedule, partial dv tiles, ragged N, gamma in {0, 1} and
+    near 1), with s_in / s_out, against the seeded f64 blocked oracle."""
+    from paper_2501_02573_b200 import ops
+    rng = np.random.default_rng(1000 + seed)
+    dk = int(rng.choice([8, 24, 64, 128, 256]))
+    dv = int(rng.choice([8, 40, 64, 128, 192, 256]))
+    B = int(rng.integers(1, 4))
+    H = int(rng.choice([1, 2, 3, 5, 40, 100]))
+    N = int(rng.choice([1, 17, 64, 100, 333, 1024, 2500]))
+    if B * H * N * (dk + dv) > 4e7:             # keep the f64 oracle to a second or two
+        N = max(1, int(4e7 // (B * H * (dk + dv))))
+    gam = [float(rng.choice([0.0, 1.0, 0.5, 1 - 2.0 ** -6, 1 - 2.0 ** -14])) for _ in range(H)]
+    b, c, v = orc.gen_inputs(B, H, N, dk, dv, np.float32, seed)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    s0 = rng.standard_normal((B, H, dk, dv)).astype(np.float32) * 0.05
+    ref, ref_s = orc.seeded_blocked_attn(b, c, v, gam, True, s0.astype(np.float64), block=64)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    for dt, kernel, tol in ((torch.bfloat16, "auto", TOL_BF16), (torch.float32, "simt", TOL_F32)):
+        s_out = torch.full((B, H, dk, dv), float("nan"), device="cuda")
+        out = ops.prefill(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_in=dev(s0), s_out=s_out, kernel=kernel)
+        assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= tol, (dt, B, H, N, dk, dv)
+        assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= max(tol, 5e-3), (dt, B, H, N, dk, dv)
