@@ -213,21 +213,18 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
     }
     cudaGetLastError();  // no workspace: run unsplit
   }
-  // more units than SMs and a mostly empty last wave: one persistent CTA per SM over equal chunk
-  // ranges (sequence heads hand their end state to the next range).  A last wave more than half
-  // full already streams near the HBM roofline (each CTA is bound by its own serial chunk chain,
-  // so fewer CTAs each go faster), and there the plain grid is kept.
+  // more units than resident CTAs and a poorly filled last wave: one persistent CTA (dk = 256: one
+  // two-CTA cluster) per slot over equal chunk ranges, sequence heads handing their end state to
+  // the next range (tc_balance_ctas has the criteria).
   // LINATTN_BALANCE=0 / 1: never / whenever the units are not a whole number of waves (dev A/B).
   static const int balance_env = getenv("LINATTN_BALANCE") ? atoi(getenv("LINATTN_BALANCE")) : -1;
-  const int64_t units = s.B * s.H * ceil_div(s.dv, 128);
   const int ctas = sm_count();
-  const int64_t rem = units % ctas;
-  const bool balance = balance_env < 0 ? (rem != 0 && 2 * rem <= ctas) : (balance_env > 0 && rem != 0);
-  if (tc && balance && s.dk <= 128 && units > ctas) {
+  const int bctas = tc && balance_env != 0 ? tc_balance_ctas(s, ctas, balance_env) : 0;
+  if (bctas > 0) {
     void* ws = nullptr;
     cudaMemPool_t pool = work_pool();
-    if (pool && cudaMallocFromPoolAsync(&ws, balance_workspace_bytes(s, ctas), pool, st) == cudaSuccess) {
-      cudaError_t e = launch_prefill_tc_balanced(q, k, v, o, log2g, s_in, s_out, s, ctas, ws, st);
+    if (pool && cudaMallocFromPoolAsync(&ws, balance_workspace_bytes(s, bctas), pool, st) == cudaSuccess) {
+      cudaError_t e = launch_prefill_tc_balanced(q, k, v, o, log2g, s_in, s_out, s, bctas, ws, st);
       cudaFreeAsync(ws, st);
       if (e != cudaErrorNotSupported) return cuda_status(e, "prefill_tc (balanced)");
     }

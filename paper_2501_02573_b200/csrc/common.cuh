@@ -91,6 +91,7 @@ struct Balance {
   int units = 0, nc = 0, w = 0, ntiles = 1;
   int chunk = 64, tile = 128;    // tokens per chunk, dv columns per unit
   float* hst = nullptr;          // [grid][dk][tile] fp32 hand-off states
+  const float* tab = nullptr;    // dk = 256 kernel: per-head gamma tables [H][65 fp32 + 192 bf16x2]
   unsigned* flags = nullptr;     // [grid] published flags, then the ticket counter (zeroed per launch)
 };
 
@@ -174,8 +175,11 @@ cudaError_t launch_state_at(const float* loc, const float* s_in, float* out, con
                             int64_t pos, const float* log2g, const ShapeArgs& s, cudaStream_t stream);
 bool tc_supported(const ShapeArgs& s, int dtype);
 
-// Balanced persistent prefill (Balance above): dk in {64, 128}, bf16, B*H*dv-tiles >= ctas.
-// `ws` holds balance_workspace_bytes(s, ctas) bytes (flags are zeroed on the stream here).
+// Balanced persistent tensor-core prefill (Balance mode 0): dk in {64, 128} (one CTA per SM) or
+// dk = 256 (two-CTA clusters).  tc_balance_ctas = grid of a balanced launch for this shape, 0 when
+// the plain grid is kept (env: LINATTN_BALANCE, -1 auto / 1 whenever the units do not fill whole
+// waves).  `ws` holds balance_workspace_bytes(s, ctas) bytes (flags are zeroed on the stream).
+int tc_balance_ctas(const ShapeArgs& s, int sms, int env);
 size_t balance_workspace_bytes(const ShapeArgs& s, int ctas);
 cudaError_t launch_prefill_tc_balanced(const void* q, const void* k, const void* v, void* o,
                                        const float* log2g, const float* s_in, float* s_out,

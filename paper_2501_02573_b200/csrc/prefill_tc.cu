@@ -667,13 +667,16 @@ struct Lazy {
 // rank).  Each CTA loads KB/MC of the 64-column Q/K boxes and multicasts them to all MC CTAs, so
 // L2 -> SM traffic for Q/K drops MC-fold; a stage is refilled only once every CTA released it
 // (tcgen05.commit multicast into each CTA's `empty`, arrival count MC).
-template <int DK, int STAGES, int MC>
+// BAL: balanced persistent schedule over cluster ranges (Balance mode 0: unit = (b*h, group of MC
+// dv tiles), tile = MC*128, hand-off slots per CTA = ticket*MC + cluster rank, gamma tables per
+// head in global memory because three roles read them across item boundaries).
+template <int DK, int STAGES, int MC, bool BAL>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                              const float* __restrict__ log2g, const float* __restrict__ s_in,
                              float* __restrict__ s_out, int H, int N, int dv, int state_only,
-                             const SegArgs sa, unsigned long long* __restrict__ trace) {
+                             const SegArgs sa, const Balance bal, unsigned long long* __restrict__ trace) {
   using G = Cfg<DK, STAGES>;
   static_assert(DK % 128 == 0 && kDVT == 128, "layout: two state warps per TMEM subpartition");
   static_assert(G::KB % MC == 0, "Q/K boxes split evenly over the cluster");
@@ -703,22 +706,31 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
-  const int bh = blockIdx.y;
-  const int j0 = blockIdx.x * kDVT;
-  int lo, hi;
-  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
-  const int nchunks = hi > lo ? (hi - lo + kC - 1) / kC : 0;
   const size_t per_state = (size_t)gridDim.y * DK * dv;
-  const float lg = log2g[bh % H];
+  int* wl = reinterpret_cast<int*>(tmem_slot + 2);   // BAL: ticket of this cluster's range
 
-  if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
-  if (threadIdx.x < 192) {
-    const int k = (int)threadIdx.x - 64;
-    const float a = k >= 0 ? gpow(lg, (float)k) : 0.f;
-    const float b = k + 1 >= 0 ? gpow(lg, (float)(k + 1)) : 0.f;
-    pw2[k] = pack_bf16x2(a, b);
+  if constexpr (!BAL) {
+    const float lg0 = log2g[blockIdx.y % H];
+    if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg0, (float)threadIdx.x);
+    if (threadIdx.x < 192) {
+      const int k = (int)threadIdx.x - 64;
+      const float a = k >= 0 ? gpow(lg0, (float)k) : 0.f;
+      const float b = k + 1 >= 0 ? gpow(lg0, (float)(k + 1)) : 0.f;
+      pw2[k] = pack_bf16x2(a, b);
+    }
   }
   if (warp == 2 && lane == 0) {
+    if constexpr (BAL) {
+      // one ticket per cluster (start order), broadcast to every CTA of the cluster
+      if (MC == 1 || cluster_ctarank() == 0) {
+        const unsigned t = atomicAdd(bal.flags + gridDim.x, 1u);
+        if constexpr (MC == 1) {
+          *wl = (int)t;
+        } else {
+          for (uint32_t r = 0; r < (uint32_t)MC; ++r) st_shared_cluster_u32(smem_u32(wl), r, t);
+        }
+      }
+    }
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], MC);
@@ -751,27 +763,67 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   const uint32_t crank = MC > 1 ? cluster_ctarank() : 0;
+  // work list: the unit of blockIdx (SegArgs segment blockIdx.z), or this cluster's range
+  auto item = [&](int k) {
+    WorkItem w;
+    if constexpr (BAL) {
+      const int t = *reinterpret_cast<volatile int*>(wl);
+      long long a = 0, b = 0;
+      balance_items(bal, t, a, b);
+      w = balance_item(bal, N, t, k, a, b);
+      w.j0 += (int)crank * kDVT;
+      if (w.in_slot >= 0) w.in_slot = w.in_slot * MC + (int)crank;
+      if (w.out_slot >= 0) w.out_slot = w.out_slot * MC + (int)crank;
+    } else {
+      w.bh = blockIdx.y;
+      w.j0 = blockIdx.x * kDVT;
+      seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, w.lo, w.hi);
+      w.in_slot = w.out_slot = -1;
+    }
+    return w;
+  };
+  int nitems = 1;
+  if constexpr (BAL) {
+    long long a = 0, b = 0;
+    nitems = balance_items(bal, *reinterpret_cast<volatile int*>(wl), a, b);
+  }
+  auto tables = [&](int bh_, const float*& pwv, const uint32_t*& pw2v) {
+    if constexpr (BAL) {
+      const float* tb = bal.tab + (size_t)(bh_ % H) * 257;
+      pwv = tb;
+      pw2v = reinterpret_cast<const uint32_t*>(tb + 65) + 64;
+    } else {
+      pwv = pw;
+      pw2v = pw2;
+    }
+  };
   // debug: per-chunk clock64 of CTA (0,0,0), trace[event * 4096 + chunk]
-  const bool tracing = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  const bool tracing = trace != nullptr && !BAL && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
 #define V3_TRACE(ev, c) do { if (tracing && lane == 0 && (c) < 4096) trace[(ev) * 4096 + (c)] = clock64(); } while (0)
 
   if (warp < 2) {
     // ------------------------------------------------------------ V' and P^T mask (TMEM lanes 0-63)
     const int srow = warp * 32 + lane;
-    Lazy lz;
-    for (int c = 0; c < nchunks; ++c) {
+    int c = 0;                                     // chunk counter over the whole work list
+    for (int it = 0; it < nitems; ++it) {
+     const WorkItem w = item(it);
+     const float* pwv;
+     const uint32_t* pw2v;
+     tables(w.bh, pwv, pw2v);
+     Lazy lz;
+     for (int t0 = w.lo; t0 < w.hi; t0 += kC, ++c) {
       const int s = c % STAGES;
-      const int L = min(kC, hi - lo - c * kC);
+      const int L = min(kC, w.hi - t0);
       mbar_wait(&vfull[c % VST], (c / VST) & 1);
       if (c > 0) {
         mbar_wait(mma_s_bar, (c - 1) & 1);           // S update c-1 has consumed V'
         tc_fence_after();
       }
       if (warp == 0) V3_TRACE(12, c);
-      lz.step(pw[L]);
+      lz.step(pwv[L]);
       {   // V'[s] = gamma^(L-1-s) V[s] / sig_{c+1}, 0 past L (row srow, both 64-column blocks)
-        const float w = srow < L ? pw[L - 1 - srow] * lz.vfac : 0.f;
-        scale_row_blocks<kDVT / 64>(smem + G::OFF_V + (c % VST) * G::V_BYTES, vs_smem, srow, 0, pack_bf16x2(w, w));
+        const float wv = srow < L ? pwv[L - 1 - srow] * lz.vfac : 0.f;
+        scale_row_blocks<kDVT / 64>(smem + G::OFF_V + (c % VST) * G::V_BYTES, vs_smem, srow, 0, pack_bf16x2(wv, wv));
       }
       fence_proxy_async_smem();
       mbar_arrive(&vs_bar[s]);
@@ -790,12 +842,12 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         if (warp == 0 && half == 0) V3_TRACE(2, c);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int t0 = half * 32 + 8 * j;
+          const int tc = half * 32 + 8 * j;
           uint4 pk;
-          pk.x = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 0], p[8 * j + 1]), pw2[t0 + 0 - srow]);
-          pk.y = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 2], p[8 * j + 3]), pw2[t0 + 2 - srow]);
-          pk.z = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 4], p[8 * j + 5]), pw2[t0 + 4 - srow]);
-          pk.w = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 6], p[8 * j + 7]), pw2[t0 + 6 - srow]);
+          pk.x = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 0], p[8 * j + 1]), pw2v[tc + 0 - srow]);
+          pk.y = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 2], p[8 * j + 3]), pw2v[tc + 2 - srow]);
+          pk.z = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 4], p[8 * j + 5]), pw2v[tc + 4 - srow]);
+          pk.w = v2::hmul2_bf16(pack_bf16x2(p[8 * j + 6], p[8 * j + 7]), pw2v[tc + 6 - srow]);
           *reinterpret_cast<uint4*>(row + (((half * 4 + j) ^ (srow & 7)) << 4)) = pk;
         }
       }
@@ -804,6 +856,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       mbar_arrive(&pt_bar[s]);
       if (warp == 0) V3_TRACE(14, c);
       if (warp == 0) V3_TRACE(6, c);
+     }
     }
   } else if (warp >= 12) {
     // ------------------------------------------------------------ V', Q' scaling and outputs
@@ -815,7 +868,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     const int mrow = lane & 7;
     const int mi = lane >> 3;
     // O^T (TMEM, lane = dv row) -> bf16 -> smem [t][d] (stmatrix.trans, 128B swizzle) -> TMA store
-    auto drain_outputs = [&](int c) {
+    auto drain_outputs = [&](int c, int t0, const WorkItem& w) {
       mbar_wait(mma_o_bar, c & 1);
       tc_fence_after();
       if (sub == 0) V3_TRACE(13, c);
@@ -852,19 +905,21 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       fence_proxy_async_smem();
       named_bar_sync(2, 128);
       if (leader) {
-        tma_store_3d(&tm_o, ot_smem, j0, lo + c * kC, bh);
-        tma_store_3d(&tm_o, ot_smem + kC * 128, j0 + 64, lo + c * kC, bh);
+        tma_store_3d(&tm_o, ot_smem, w.j0, t0, w.bh);
+        tma_store_3d(&tm_o, ot_smem + kC * 128, w.j0 + 64, t0, w.bh);
         bulk_commit();
       }
     };
-    Lazy lz;
-    for (int c = 0; c < (state_only ? 0 : nchunks); ++c) {
-      const int s = c % STAGES;
-      const int L = min(kC, hi - lo - c * kC);
-      uint8_t* stage = smem + s * G::STAGE_BYTES;
-      (void)stage;
-      (void)s;
-      lz.step(pw[L]);
+    int c = 0;
+    for (int it = 0; it < (state_only ? 0 : nitems); ++it) {
+     const WorkItem w = item(it);
+     const float* pwv;
+     const uint32_t* pw2v;
+     tables(w.bh, pwv, pw2v);
+     Lazy lz;
+     for (int t0 = w.lo; t0 < w.hi; t0 += kC, ++c) {
+      const int L = min(kC, w.hi - t0);
+      lz.step(pwv[L]);
       {
         // O_inter(c)[d][t] *= sig_c gamma^(t+1)  (fp32, in TMEM: lanes sub*32.., columns t)
         mbar_wait(ox_bar, c & 1);
@@ -876,7 +931,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
           tmem_ld32(ta_o + half * 32, o);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] *= lz.sig_c * pw[half * 32 + i + 1];
+          for (int i = 0; i < 32; ++i) o[i] *= lz.sig_c * pwv[half * 32 + i + 1];
           tmem_st32(ta_o + half * 32, o);
         }
         tmem_wait_st();
@@ -884,7 +939,8 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         mbar_arrive(ox_scaled);
         if (sub == 0) V3_TRACE(6, c);
       }
-      drain_outputs(c);
+      drain_outputs(c, t0, w);
+     }
     }
     if (leader) bulk_wait<0>();
   } else if (warp >= 4) {
@@ -892,32 +948,66 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     // warp (half, sub): TMEM lanes sub*32.. (dv rows), state columns [half*SCOL, +SCOL)
     const int sub = (warp - 4) % 4;
     const int col0 = ((warp - 4) / 4) * SCOL;
-    const int jd = j0 + sub * 32 + lane;
-    const bool dv_ok = jd < dv;
+    const int d = sub * 32 + lane;                       // dv row within the 128-wide tile
     const uint32_t ta_s = tbase + ((sub * 32) << 16) + T_S + col0;
     const uint32_t ta_sb = tbase + ((sub * 32) << 16) + T_SB + col0 / 2;
-    float* const so = (s_out && dv_ok && (state_only || blockIdx.z == gridDim.z - 1))
-                          ? s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)bh * DK + col0) * dv + jd
-                          : nullptr;
+    const bool leader = (warp == 4 && lane == 0);
+    int c = 0;
+    for (int it = 0; it < nitems; ++it) {
+    const WorkItem w = item(it);
+    const float* pwv;
+    const uint32_t* pw2v;
+    tables(w.bh, pwv, pw2v);
+    const float lg = log2g[w.bh % H];
+    const int jd = w.j0 + d;
+    const bool dv_ok = jd < dv;
+    const int nch = w.hi > w.lo ? (w.hi - w.lo + kC - 1) / kC : 0;
+    // end state: a balanced head publishes it to its hand-off slot; otherwise state-only launches
+    // write one local state per segment, full launches only the segment ending the sequence
+    float* so = nullptr;
+    size_t so_stride = dv;
+    if (BAL && w.out_slot >= 0) {
+      if (dv_ok) so = bal.hst + ((size_t)w.out_slot * DK + col0) * kDVT + d;
+      so_stride = kDVT;
+    } else if (s_out && dv_ok && (BAL ? w.hi == N : (state_only || blockIdx.z == gridDim.z - 1))) {
+      so = s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)w.bh * DK + col0) * dv + jd;
+    }
+    if (it > 0) {
+      // the previous item's last S update and O_inter are done before T is re-seeded
+      mbar_wait(state_only ? mma_s_bar : ox_bar, (c - 1) & 1);
+      tc_fence_after();
+    }
+    if (BAL && w.in_slot >= 0) {
+      if (leader)
+        while (ld_acquire_gpu(bal.flags + w.in_slot) == 0u) __nanosleep(256);
+      named_bar_sync(3, 256);
+    }
     {
-      // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs)
-      const float w_in = gpow(lg, (float)lo);
+      // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs), or a
+      // balanced tail's hand-off state (s_in and every earlier token already folded in)
+      const float w_in = gpow(lg, (float)w.lo);
       for (int cb = 0; cb < SCOL / 32; ++cb) {
         float sv[32];
+        if (BAL && w.in_slot >= 0) {
+          const float* hp = bal.hst + ((size_t)w.in_slot * DK + col0 + cb * 32) * kDVT + d;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          sv[i] = (s_in && dv_ok) ? w_in * s_in[((size_t)bh * DK + col0 + cb * 32 + i) * dv + jd] : 0.f;
-        for (int qi = 0; qi < sa.nloc; ++qi) {
-          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
-          if (wq < 0.f || !dv_ok) continue;
-          const float* lq = sa.loc + qi * per_state + ((size_t)bh * DK + col0 + cb * 32) * dv + jd;
+          for (int i = 0; i < 32; ++i) sv[i] = dv_ok ? __ldcg(hp + (size_t)i * kDVT) : 0.f;
+        } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sv[i] = fmaf(wq, lq[(size_t)i * dv], sv[i]);
+          for (int i = 0; i < 32; ++i)
+            sv[i] = (s_in && dv_ok) ? w_in * s_in[((size_t)w.bh * DK + col0 + cb * 32 + i) * dv + jd] : 0.f;
+          for (int qi = 0; qi < sa.nloc; ++qi) {
+            const float wq = seg_loc_weight(sa, qi, N, w.lo, lg);
+            if (wq < 0.f || !dv_ok) continue;
+            const float* lq = sa.loc + qi * per_state + ((size_t)w.bh * DK + col0 + cb * 32) * dv + jd;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sv[i] = fmaf(wq, lq[(size_t)i * dv], sv[i]);
+          }
         }
-        if (nchunks == 0) {
+        if (nch == 0) {
           if (so) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = sv[i];
+            for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * so_stride] = sv[i];
           }
         } else {
           tmem_st32(ta_s + cb * 32, sv);
@@ -926,8 +1016,8 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       tmem_wait_st();
     }
     Lazy lz;
-    for (int c = 0; c < nchunks; ++c) {
-      const int L = min(kC, hi - lo - c * kC);
+    for (int t0 = w.lo; t0 < w.hi; t0 += kC, ++c) {
+      const int L = min(kC, w.hi - t0);
       if (c > 0) {
         // S_c complete; in the full pass also O_inter(c-1) done (it follows the S update in
         // the pipe), so the bf16 operand buffer is free and S_c can be published straight away
@@ -935,7 +1025,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         tc_fence_after();
       }
       if (warp == 4) V3_TRACE(0, c);
-      lz.step(pw[L]);
+      lz.step(pwv[L]);
       // publish bf16 T_c for O_inter(c); rewrite T only when renormalising (T <- sig gamma^L T)
       if (!state_only || lz.renorm) {
 #pragma unroll 1
@@ -961,23 +1051,32 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       mbar_arrive(st_done);
       if (warp == 4) V3_TRACE(1, c);
     }
-    if (nchunks > 0 && so) {
-      mbar_wait(mma_s_bar, (nchunks - 1) & 1);
+    if (nch > 0 && so) {
+      mbar_wait(mma_s_bar, (c - 1) & 1);
       tc_fence_after();
       for (int cb = 0; cb < SCOL / 32; ++cb) {
         float sv[32];
         tmem_ld32(ta_s + cb * 32, sv);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * dv] = lz.sig * sv[i];   // S = sig T
+        for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * so_stride] = lz.sig * sv[i];   // S = sig T
       }
     }
+    if (BAL && w.out_slot >= 0) {                 // release the hand-off to the next range's tail
+      __threadfence();
+      named_bar_sync(4, 256);
+      if (leader) st_release_gpu(bal.flags + w.out_slot, 1u);
+    }
+    }  // work items
   } else if (warp == 2) {
     // ------------------------------------------------------------ TMA producer
     // lane 0 streams the Q/K ring, lane 1 the V ring (independent waits)
     if (lane == 0) {
       const uint32_t bytes = (state_only ? 0 : G::Q_BYTES) + G::K_BYTES;
-      for (int c = 0; c < nchunks; ++c) {
+      int c = 0;
+      for (int it = 0; it < nitems; ++it) {
+       const WorkItem w = item(it);
+       for (int t0 = w.lo; t0 < w.hi; t0 += kC, ++c) {
         const int s = c % STAGES;
         mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);   // every CTA of the cluster released s
         V3_TRACE(9, c);
@@ -987,27 +1086,33 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         for (int j = 0; j < G::KB / MC; ++j) {
           const int kb = (int)crank * (G::KB / MC) + j;
           if constexpr (MC > 1) {
-            if (!state_only) tma_load_3d_mc(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh, kMask);
-            tma_load_3d_mc(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh, kMask);
+            if (!state_only) tma_load_3d_mc(st + kb * 8192, &tm_q, &full[s], kb * 64, t0, w.bh, kMask);
+            tma_load_3d_mc(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, t0, w.bh, kMask);
           } else {
-            if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, lo + c * kC, bh);
-            tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, lo + c * kC, bh);
+            if (!state_only) tma_load_3d(st + kb * 8192, &tm_q, &full[s], kb * 64, t0, w.bh);
+            tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, t0, w.bh);
           }
         }
+       }
       }
       if constexpr (MC > 1) {   // peers' final releases have landed before this CTA may exit
-        for (int c = (nchunks > STAGES ? nchunks - STAGES : 0); c < nchunks; ++c)
-          mbar_wait(&empty[c % STAGES], (c / STAGES) & 1);
+        const int nchunks = c;
+        for (int cc = (nchunks > STAGES ? nchunks - STAGES : 0); cc < nchunks; ++cc)
+          mbar_wait(&empty[cc % STAGES], (cc / STAGES) & 1);
       }
     } else if (lane == 1) {
-      for (int c = 0; c < nchunks; ++c) {
+      int c = 0;
+      for (int it = 0; it < nitems; ++it) {
+       const WorkItem w = item(it);
+       for (int t0 = w.lo; t0 < w.hi; t0 += kC, ++c) {
         const int s = c % VST;
         mbar_wait(&vempty[s], ((c / VST) & 1) ^ 1);
         uint8_t* st = smem + G::OFF_V + s * G::V_BYTES;
         mbar_arrive_expect_tx(&vfull[s], G::V_BYTES);
 #pragma unroll
         for (int nb = 0; nb < kDVT / 64; ++nb)
-          tma_load_3d(st + nb * 8192, &tm_v, &vfull[s], j0 + nb * 64, lo + c * kC, bh);
+          tma_load_3d(st + nb * 8192, &tm_v, &vfull[s], w.j0 + nb * 64, t0, w.bh);
+       }
       }
     }
   } else {
@@ -1038,6 +1143,12 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       mma_commit_elect(mma1_bar);
       V3_TRACE(5, c);
     };
+    // the tensor pipe sees one flat chunk stream across the work list
+    int nchunks = 0;
+    for (int it = 0; it < nitems; ++it) {
+      const WorkItem w = item(it);
+      nchunks += w.hi > w.lo ? (w.hi - w.lo + kC - 1) / kC : 0;
+    }
     if (!state_only && nchunks > 0) issue_mma1(0);
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % STAGES;
@@ -1159,14 +1270,16 @@ template <int DK, int STAGES, int MC>
 cudaError_t launch_tmem_state_mc(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                                  const CUtensorMap& mo, const float* log2g, const float* s_in, float* s_out,
                                  const ShapeArgs& s, bool state_only, const SegArgs& sa, int nz,
-                                 cudaStream_t stream) {
+                                 cudaStream_t stream, const Balance& bal = Balance{}, int ctas = 0) {
   using G = v3::Cfg<DK, STAGES>;
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
-  auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC>;
+  auto kern = bal.on ? v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC, true>
+                     : v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC, false>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)(s.B * s.H), (unsigned)nz);
+  cfg.gridDim = bal.on ? dim3((unsigned)ctas)
+                       : dim3((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)(s.B * s.H), (unsigned)nz);
   cfg.blockDim = dim3(v3::kThreads);
   cfg.dynamicSmemBytes = G::SMEM;
   cfg.stream = stream;
@@ -1178,7 +1291,7 @@ cudaError_t launch_tmem_state_mc(const CUtensorMap& mq, const CUtensorMap& mk, c
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   err = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H, (int)s.N, (int)s.dv,
-                           state_only ? 1 : 0, sa, g_trace);
+                           state_only ? 1 : 0, sa, bal, g_trace);
   count_launch();
   if (err != cudaSuccess) return err;
   return cudaGetLastError();
@@ -1208,11 +1321,11 @@ int max_active_clusters(int m) {
   int n = 0;
   cudaError_t err = cudaErrorInvalidValue;
   if (m == 4) {
-    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 4>;
+    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 4, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) == cudaSuccess)
       err = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
   } else if (m == 2) {
-    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 2>;
+    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 2, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) == cudaSuccess)
       err = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
   }
@@ -1299,8 +1412,53 @@ cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void*
   }
 }
 
+namespace {
+// Per-head gamma tables of the balanced dk = 256 kernel: [H][65 fp32 gamma^n | 192 bf16x2 pairs].
+__global__ void gamma_tables_kernel(const float* __restrict__ log2g, float* __restrict__ tab) {
+  const float lg = log2g[blockIdx.x];
+  float* t = tab + (size_t)blockIdx.x * 257;
+  uint32_t* t2 = reinterpret_cast<uint32_t*>(t + 65);
+  for (int n = threadIdx.x; n <= kC; n += blockDim.x) t[n] = gpow(lg, (float)n);
+  for (int i = threadIdx.x; i < 192; i += blockDim.x) {
+    const int k = i - 64;
+    t2[i] = pack_bf16x2(k >= 0 ? gpow(lg, (float)k) : 0.f, k + 1 >= 0 ? gpow(lg, (float)(k + 1)) : 0.f);
+  }
+}
+size_t flags_bytes(int ctas) { return 256 * (size_t)((ctas + 1 + 63) / 64); }
+size_t tab_bytes(const ShapeArgs& s) { return s.dk == 256 ? 256 * (size_t)((s.H * 257 * 4 + 255) / 256) : 0; }
+}  // namespace
+
+int tc_balance_ctas(const ShapeArgs& s, int sms, int env) {
+  const int64_t tiles = (s.dv + kDVT - 1) / kDVT;
+  if (s.dk <= 128) {
+    const int64_t units = s.B * s.H * tiles, rem = units % sms;
+    if (units <= sms || rem == 0) return 0;
+    // a last wave more than half full already streams near the HBM roofline (each CTA is bound
+    // by its own serial chunk chain, so fewer CTAs each go faster)
+    return (env > 0 || 2 * rem <= sms) ? sms : 0;
+  }
+  if (s.dk != 256 || tiles % 2 != 0) return 0;
+  // dk = 256: ranges over clusters of two CTAs (74 co-resident pairs, all SMs) against the
+  // plain grid's whole waves of the best cluster size (33 co-resident quads)
+  const int slots2 = max_active_clusters<256, 2>(2);
+  if (slots2 <= 0) return 0;
+  const int64_t pairs = s.B * s.H * tiles / 2;
+  if (pairs <= slots2 || pairs % slots2 == 0) return 0;
+  int64_t plain = (pairs + slots2 - 1) / slots2;
+  if (tiles % 4 == 0) {
+    const int slots4 = max_active_clusters<256, 2>(4);
+    if (slots4 > 0) plain = std::min<int64_t>(plain, (pairs / 2 + slots4 - 1) / slots4);
+  }
+  // measured (1 x H x 16384, dv = 512): a wave of 33 quads 0.41 ms, of 74 pairs 0.45 ms, and the
+  // balanced ranges cost ~11 % over the pairs' steady state (item switches, hand-offs), so the
+  // balanced launch wins when its fractional waves stay under 0.75 of the plain whole waves
+  // (H = 40: 0.72 -> 0.54 ms, H = 48: 0.74 -> 0.65 ms; H = 56 and configs[2] (H = 64) stay plain)
+  const double bal = (double)pairs / slots2;
+  return (env > 0 || bal < 0.75 * (double)plain) ? 2 * slots2 : 0;
+}
+
 size_t balance_workspace_bytes(const ShapeArgs& s, int ctas) {
-  return 256 * (size_t)((ctas + 1 + 63) / 64) + (size_t)ctas * s.dk * kDVT * sizeof(float);
+  return flags_bytes(ctas) + tab_bytes(s) + (size_t)ctas * s.dk * kDVT * sizeof(float);
 }
 
 cudaError_t launch_prefill_tc_balanced(const void* q, const void* k, const void* v, void* o,
@@ -1308,24 +1466,43 @@ cudaError_t launch_prefill_tc_balanced(const void* q, const void* k, const void*
                                        const ShapeArgs& s, int ctas, void* ws, cudaStream_t stream) {
   for (const void* p : {q, k, v, (const void*)o})
     if (reinterpret_cast<uintptr_t>(p) & 15) return cudaErrorNotSupported;
+  const int mc = s.dk == 256 ? 2 : 1;                      // CTAs per cluster (one range each)
   const int64_t ntiles = (s.dv + kDVT - 1) / kDVT;
-  const int64_t units = s.B * s.H * ntiles, nc = (s.N + kC - 1) / kC;
-  const int64_t w = (units * nc + ctas - 1) / ctas;
-  if ((s.dk != 64 && s.dk != 128) || w < nc || units * nc > (1LL << 31) - 1) return cudaErrorNotSupported;
+  if (ntiles % mc != 0 || ctas % mc != 0) return cudaErrorNotSupported;
+  const int64_t units = s.B * s.H * (ntiles / mc), nc = (s.N + kC - 1) / kC;
+  const int ranges = ctas / mc;
+  const int64_t w = (units * nc + ranges - 1) / ranges;
+  if ((s.dk != 64 && s.dk != 128 && s.dk != 256) || w < nc || units * nc > (1LL << 31) - 1)
+    return cudaErrorNotSupported;
   Balance bal;
   bal.on = 1;
   bal.units = (int)units;
   bal.nc = (int)nc;
   bal.w = (int)w;
-  bal.ntiles = (int)ntiles;
-  bal.flags = static_cast<unsigned*>(ws);
-  bal.hst = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256 * (size_t)((ctas + 1 + 63) / 64));
-  const int used = (int)((units * nc + w - 1) / w);     // ranges that hold work
+  bal.ntiles = (int)(ntiles / mc);
+  bal.tile = mc * kDVT;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  bal.flags = reinterpret_cast<unsigned*>(base);
+  float* tab = reinterpret_cast<float*>(base + flags_bytes(ctas));
+  bal.tab = tab;
+  bal.hst = reinterpret_cast<float*>(base + flags_bytes(ctas) + tab_bytes(s));
+  const int used = (int)((units * nc + w - 1) / w) * mc;   // CTAs whose range holds work
   cudaError_t err = cudaMemsetAsync(ws, 0, sizeof(unsigned) * (ctas + 1), stream);
   if (err != cudaSuccess) return err;
   if (s.dk == 64)
     return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, false, SegArgs{}, 1, stream, bal, used);
-  return launch_pipe<128, V2_STAGES128>(q, k, v, o, log2g, s_in, s_out, s, false, SegArgs{}, 1, stream, bal, used);
+  if (s.dk == 128)
+    return launch_pipe<128, V2_STAGES128>(q, k, v, o, log2g, s_in, s_out, s, false, SegArgs{}, 1, stream, bal, used);
+  gamma_tables_kernel<<<(unsigned)s.H, 64, 0, stream>>>(log2g, tab);
+  count_launch();
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  CUtensorMap mq, mk, mv, mo;
+  const int64_t BH = s.B * s.H;
+  if (!make_map(&mk, k, s.dk, s.N, BH) || !make_map(&mv, v, s.dv, s.N, BH) || !make_map(&mq, q, s.dk, s.N, BH) ||
+      !make_map(&mo, o, s.dv, s.N, BH))
+    return cudaErrorInvalidValue;
+  return launch_tmem_state_mc<256, 2, 2>(mq, mk, mv, mo, log2g, s_in, s_out, s, false, SegArgs{}, 1, stream, bal,
+                                          used);
 }
 
 }  // namespace linattn

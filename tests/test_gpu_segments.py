@@ -207,11 +207,13 @@ def test_long_context_gamma_near_one(ops):
         assert orc.max_rel_error(o[0, h, N - T:].float().cpu().numpy(), ref[0, 0]) <= TOL_BF16
 
 
-@pytest.mark.parametrize("B,H,dk,dv", [(2, 80, 128, 128), (1, 75, 64, 256), (3, 53, 128, 192)])
+@pytest.mark.parametrize("B,H,dk,dv", [(2, 80, 128, 128), (1, 75, 64, 256), (3, 53, 128, 192),
+                                       (1, 40, 256, 512), (3, 30, 256, 256)])
 @pytest.mark.parametrize("N", [1, 64, 200, 1000])
 def test_balanced_schedule(ops, B, H, dk, dv, N):
     """More units than SMs (not a whole number of waves) runs the balanced persistent schedule:
-    sequence heads publish their end state to the next CTA's range.  Checked with s_in seeding
+    sequence heads publish their end state to the next CTA's range (dk = 256: to the same cluster
+    rank of the next two-CTA cluster's range).  Checked with s_in seeding
     and s_out against the seeded f64 blocked oracle, gamma in {0, 1} included."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     units = B * H * -(-dv // 128)

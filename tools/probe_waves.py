@@ -10,7 +10,8 @@ for H in [int(h) for h in (sys.argv[2] if len(sys.argv) > 2 else "16,32,36,37,40
     v = torch.randn(1, H, N, dv, device="cuda", dtype=torch.bfloat16)
     out = torch.empty_like(v)
     l2 = ops.log2_gamma([0.99] * H, True, "cuda")
-    f = lambda: ops.prefill(q, k, v, l2, out=out, seq_split=1)
+    kw = {} if os.environ.get("PROBE_AUTO") else {"seq_split": 1}
+    f = lambda: ops.prefill(q, k, v, l2, out=out, **kw)
     for _ in range(3): f()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
