@@ -721,14 +721,12 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
   }
   if (warp == 2 && lane == 0) {
     if constexpr (BAL) {
-      // one ticket per cluster (start order), broadcast to every CTA of the cluster
+      // one ticket per cluster (start order); rank 0 takes it and parks it in global memory for
+      // the other ranks, which read it after the cluster barrier below
       if (MC == 1 || cluster_ctarank() == 0) {
         const unsigned t = atomicAdd(bal.flags + gridDim.x, 1u);
-        if constexpr (MC == 1) {
-          *wl = (int)t;
-        } else {
-          for (uint32_t r = 0; r < (uint32_t)MC; ++r) st_shared_cluster_u32(smem_u32(wl), r, t);
-        }
+        if constexpr (MC == 1) *wl = (int)t;
+        else bal.flags[gridDim.x + 1 + blockIdx.x / MC] = t;
       }
     }
     for (int i = 0; i < STAGES; ++i) {
@@ -760,6 +758,10 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
   tc_fence_before();
   __syncthreads();
   if constexpr (MC > 1) cluster_sync_all();   // peers' barriers exist before any multicast
+  if constexpr (BAL && MC > 1) {
+    if (threadIdx.x == 0) *wl = (int)__ldcg(bal.flags + gridDim.x + 1 + blockIdx.x / MC);
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   const uint32_t crank = MC > 1 ? cluster_ctarank() : 0;
@@ -1424,7 +1426,8 @@ __global__ void gamma_tables_kernel(const float* __restrict__ log2g, float* __re
     t2[i] = pack_bf16x2(k >= 0 ? gpow(lg, (float)k) : 0.f, k + 1 >= 0 ? gpow(lg, (float)(k + 1)) : 0.f);
   }
 }
-size_t flags_bytes(int ctas) { return 256 * (size_t)((ctas + 1 + 63) / 64); }
+// [ctas] hand-off flags, the ticket counter, then [ctas] per-cluster ticket slots
+size_t flags_bytes(int ctas) { return 256 * (size_t)((2 * ctas + 1 + 63) / 64); }
 size_t tab_bytes(const ShapeArgs& s) { return s.dk == 256 ? 256 * (size_t)((s.H * 257 * 4 + 255) / 256) : 0; }
 }  // namespace
 

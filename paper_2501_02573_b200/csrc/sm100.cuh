@@ -121,13 +121,6 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   return v;
 }
 
-// Store a u32 into the same shared-memory offset of CTA `rank` of this cluster (DSMEM).
-__device__ __forceinline__ void st_shared_cluster_u32(uint32_t local_addr, uint32_t rank, uint32_t v) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(remote), "r"(v) : "memory");
-}
-
 // Four transposed 8x8 b16 tiles from mma-fragment registers into shared memory.
 __device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, uint32_t r0, uint32_t r1, uint32_t r2,
                                                   uint32_t r3) {

@@ -29,5 +29,10 @@ for dk in (128, 64):
     l2 = ops.log2_gamma([0.9] * H, True, "cuda")
     ops.prefill(q, k, v, l2, s_in=torch.zeros(1, H, dk, 128, device="cuda"),
                 s_out=torch.empty(1, H, dk, 128, device="cuda"))
+# dk = 256 balanced schedule over two-CTA clusters (80 pairs > 74 co-resident)
+q = torch.randn(1, 40, 200, 256, device="cuda", dtype=torch.bfloat16)
+k = torch.randn_like(q)
+v = torch.randn(1, 40, 200, 512, device="cuda", dtype=torch.bfloat16)
+ops.prefill(q, k, v, ops.log2_gamma([0.9] * 40, True, "cuda"), s_out=torch.empty(1, 40, 256, 512, device="cuda"))
 torch.cuda.synchronize()
 print("sanitize driver done")
