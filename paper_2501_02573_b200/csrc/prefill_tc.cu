@@ -164,6 +164,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  if constexpr (!BAL) pdl_wait();   // everything above overlapped the previous kernel's tail
   // work list: the one unit of blockIdx (SegArgs segment blockIdx.z), or this ticket's range
   const int nitems = BAL ? wl[1] : 1;
   auto item = [&](int k) {
@@ -1261,9 +1262,15 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   if (err != cudaSuccess) return err;
   const dim3 grid = bal.on ? dim3((unsigned)ctas)
                            : dim3((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
-  kern<<<grid, v2::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out,
-                                                (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
-                                                sa, bal, g_trace);
+  if (bal.on) {   // the balanced launch follows the memset of its flags: plain stream order
+    kern<<<grid, v2::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out,
+                                                  (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
+                                                  sa, bal, g_trace);
+  } else {
+    err = launch_pdl(kern, grid, dim3(v2::kThreads), G::SMEM, stream, mq, mk, mv, mo, log2g, s_in, s_out,
+                     (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0, sa, bal, g_trace);
+    if (err != cudaSuccess) return err;
+  }
   count_launch();
   return cudaGetLastError();
 }

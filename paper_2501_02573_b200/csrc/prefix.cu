@@ -21,6 +21,7 @@ struct SegLens {
 __global__ void prefix_combine_kernel(const float4* __restrict__ gathered, float4* __restrict__ s_in,
                                       SegLens lens, int rank, const float* __restrict__ log2g,
                                       int H, int64_t per_head4, int64_t per_rank4) {
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= per_rank4) return;
   const int h = (int)((idx / per_head4) % H);
@@ -47,6 +48,7 @@ __global__ void prefix_combine_kernel(const float4* __restrict__ gathered, float
 __global__ void prefix_combine_kernel_scalar(const float* __restrict__ gathered, float* __restrict__ s_in,
                                              SegLens lens, int rank, const float* __restrict__ log2g,
                                              int H, int64_t per_head, int64_t per_rank) {
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= per_rank) return;
   const int h = (int)((idx / per_head) % H);
@@ -69,6 +71,7 @@ __global__ void state_at_kernel(const float4* __restrict__ loc, const float4* __
                                 float4* __restrict__ out, const SegArgs sa, int N, int pos,
                                 const float* __restrict__ log2g, int H, int64_t per_head4,
                                 int64_t per_state4) {
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= per_state4) return;
   const float lg = log2g[(int)((idx / per_head4) % H)];
@@ -104,6 +107,7 @@ __global__ void segment_prefix_kernel(const float4* __restrict__ loc, float4* __
                                       const SegArgs sa, int N, int seg_len, int nseg,
                                       const float* __restrict__ log2g, int H, int64_t per_head4,
                                       int64_t per_state4) {
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= per_state4) return;
   const float lg = log2g[(int)((idx / per_head4) % H)];
@@ -149,11 +153,12 @@ cudaError_t launch_segment_prefix(const SegArgs& sa, float* incl, int64_t seg_le
     if (reinterpret_cast<uintptr_t>(p) & 15) return cudaErrorNotSupported;
   const int64_t n4 = s.B * s.H * per_head / 4;
   constexpr int NT = 256;
-  segment_prefix_kernel<<<(unsigned)((n4 + NT - 1) / NT), NT, 0, stream>>>(
-      (const float4*)sa.loc, (float4*)incl, sa, (int)s.N, (int)std::min<int64_t>(seg_len, 0x7fffffff),
-      (int)nseg, log2g, (int)s.H, per_head / 4, n4);
+  cudaError_t err = launch_pdl(segment_prefix_kernel, dim3((unsigned)((n4 + NT - 1) / NT)), dim3(NT), 0, stream,
+                               (const float4*)sa.loc, (float4*)incl, sa, (int)s.N,
+                               (int)std::min<int64_t>(seg_len, 0x7fffffff), (int)nseg, log2g, (int)s.H,
+                               per_head / 4, n4);
   count_launch();
-  return cudaGetLastError();
+  return err != cudaSuccess ? err : cudaGetLastError();
 }
 
 cudaError_t launch_state_at(const float* loc, const float* s_in, float* out, const SegArgs& sa,
@@ -184,8 +189,10 @@ cudaError_t launch_prefix_combine(const float* gathered, float* s_in, const int6
   constexpr int NT = 256;
   if (vec) {
     const int64_t n4 = per_rank / 4;
-    prefix_combine_kernel<<<(unsigned)((n4 + NT - 1) / NT), NT, 0, stream>>>(
-        (const float4*)gathered, (float4*)s_in, lens, rank, log2g, (int)s.H, per_head / 4, n4);
+    cudaError_t err = launch_pdl(prefix_combine_kernel, dim3((unsigned)((n4 + NT - 1) / NT)), dim3(NT), 0, stream,
+                                 (const float4*)gathered, (float4*)s_in, lens, rank, log2g, (int)s.H,
+                                 per_head / 4, n4);
+    if (err != cudaSuccess) return err;
   } else {
     prefix_combine_kernel_scalar<<<(unsigned)((per_rank + NT - 1) / NT), NT, 0, stream>>>(
         gathered, s_in, lens, rank, log2g, (int)s.H, per_head, per_rank);
