@@ -181,6 +181,7 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
   __shared__ int s_ticket;
   int ticket = 0, nitems = 1;
   long long r0 = 0, r1 = 0;
+  if constexpr (!BAL) pdl_wait();               // launched with programmatic dependent launch
   if constexpr (BAL) {
     if (tid == 0) s_ticket = (int)atomicAdd(bal.flags + gridDim.x, 1u);   // start order
     __syncthreads();
@@ -446,8 +447,14 @@ cudaError_t launch_rb(int mode, const void* q, const void* k, const void* v, voi
     using TT = typename decltype(tp)::type;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    kern<<<grid, NT, smem, stream>>>((const TT*)q, (const TT*)k, (const TT*)v, (TT*)o, log2g, s_in, s_out,
-                                     (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, state_only ? 1 : 0, sa, bal);
+    if constexpr (BAL) {   // follows the memset of its flags: plain stream order
+      kern<<<grid, NT, smem, stream>>>((const TT*)q, (const TT*)k, (const TT*)v, (TT*)o, log2g, s_in, s_out,
+                                       (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, state_only ? 1 : 0, sa, bal);
+    } else {
+      err = launch_pdl(kern, grid, dim3(NT), smem, stream, (const TT*)q, (const TT*)k, (const TT*)v, (TT*)o,
+                       log2g, s_in, s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, state_only ? 1 : 0, sa, bal);
+      if (err != cudaSuccess) return err;
+    }
     count_launch();
     return cudaGetLastError();
   };

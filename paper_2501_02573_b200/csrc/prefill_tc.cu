@@ -763,6 +763,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     if (threadIdx.x == 0) *wl = (int)__ldcg(bal.flags + gridDim.x + 1 + blockIdx.x / MC);
     __syncthreads();
   }
+  if constexpr (!BAL) pdl_wait();   // everything above overlapped the previous kernel's tail
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   const uint32_t crank = MC > 1 ? cluster_ctarank() : 0;
@@ -1292,13 +1293,15 @@ cudaError_t launch_tmem_state_mc(const CUtensorMap& mq, const CUtensorMap& mk, c
   cfg.blockDim = dim3(v3::kThreads);
   cfg.dynamicSmemBytes = G::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = MC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see pdl_wait (plain grid only)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = bal.on ? 1 : 2;
   err = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H, (int)s.N, (int)s.dv,
                            state_only ? 1 : 0, sa, bal, g_trace);
   count_launch();
