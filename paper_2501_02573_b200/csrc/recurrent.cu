@@ -1,7 +1,9 @@
 // Row-based recurrence in one launch: the reference _row_based_slice (kernels.py:93-106),
 //   for t in 0..N-1:  S <- gamma S + k_t^T v_t ;  o_t = q_t S
 // One CTA per (b*h, 128-wide dv tile) walks the tokens with its fp32 state in registers:
-// thread (row group rg, column quad cv) owns rows rg, rg+RRG, ... x columns 4cv..4cv+3.
+// thread (row group rg, column quad cv) owns the contiguous rows rg*rpt .. rg*rpt+rpt-1
+// (rpt = ceil(dk / RRG)) x columns 4cv..4cv+3, so its q and k values of a token are one
+// contiguous run in shared memory (16-byte vector loads, broadcast across the warp).
 // Tokens are staged TC at a time by cp.async one chunk ahead, and each token's o partials go to
 // a [TC][RRG][128] shared buffer that is reduced once per chunk -- two barriers per TC tokens.
 #include "common.cuh"
@@ -41,7 +43,11 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
   const int nj = min(RDV, dv - j0);
   const int tid = threadIdx.x;
   const int cv = tid % RCQ, rg = tid / RCQ;
-  const int nrows = (dk - rg + RRG - 1) / RRG;              // rows rg, rg+RRG, ... < dk
+  const int rpt = (dk + RRG - 1) / RRG;                     // rows per thread
+  const int row0 = rg * rpt;
+  const int nrows = max(0, min(rpt, dk - row0));           // rows row0 .. row0+nrows-1
+  constexpr int EV2 = 16 / sizeof(T);
+  const bool vec = (rpt % EV2) == 0;                       // 16-byte aligned runs (dk % (8*EV2) == 0)
   const float g = gpow(log2g[bh % H], 1.f);
   const T* qb = q + (size_t)bh * N * dk;
   const T* kb = k + (size_t)bh * N * dk;
@@ -54,7 +60,7 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
   for (int r = 0; r < RMAXR; ++r)
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int i = rg + r * RRG, j = 4 * cv + e;
+      const int i = row0 + r, j = 4 * cv + e;
       S[r][e] = (s_in && r < nrows && j < nj) ? s_in[((size_t)bh * dk + i) * dv + j0 + j] : 0.f;
     }
   // stage tokens [c0, c0 + TC) into buffer buf (rows past N and columns past nj are never read)
@@ -92,11 +98,26 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
 #pragma unroll
       for (int e = 0; e < 4; ++e) vv[e] = 4 * cv + e < nj ? to_f32(vc[t * RDV + 4 * cv + e]) : 0.f;
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const T* kt = kc + t * dk + row0;
+      const T* qt = qc + t * dk + row0;
 #pragma unroll
-      for (int r = 0; r < RMAXR; ++r) {
-        if (r < nrows) {
-          const int i = rg + r * RRG;
-          const float kr = to_f32(kc[t * dk + i]), qr = to_f32(qc[t * dk + i]);
+      for (int r0 = 0; r0 < RMAXR; r0 += EV2) {
+        if (r0 >= nrows) break;
+        T kb8[EV2], qb8[EV2];
+        if (vec) {   // one 16-byte load each (all lanes of the warp read the same run)
+          *reinterpret_cast<uint4*>(kb8) = *reinterpret_cast<const uint4*>(kt + r0);
+          *reinterpret_cast<uint4*>(qb8) = *reinterpret_cast<const uint4*>(qt + r0);
+        } else {
+#pragma unroll
+          for (int u = 0; u < EV2; ++u) {
+            kb8[u] = r0 + u < nrows ? kt[r0 + u] : T(0.f);
+            qb8[u] = r0 + u < nrows ? qt[r0 + u] : T(0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < EV2; ++u) {
+          const int r = r0 + u;
+          const float kr = to_f32(kb8[u]), qr = to_f32(qb8[u]);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             S[r][e] = fmaf(g, S[r][e], kr * vv[e]);
@@ -124,7 +145,7 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
     for (int r = 0; r < RMAXR; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int i = rg + r * RRG, j = 4 * cv + e;
+        const int i = row0 + r, j = 4 * cv + e;
         if (r < nrows && j < nj) s_out[((size_t)bh * dk + i) * dv + j0 + j] = S[r][e];
       }
   }
