@@ -121,18 +121,18 @@ struct WorkItem {
   int in_slot, out_slot;         // hand-off slot to seed from / publish to, -1 = none
 };
 
-__device__ __forceinline__ int balance_items(const Balance& P, int t, long long& start, long long& end) {
+__host__ __device__ __forceinline__ int balance_items(const Balance& P, int t, long long& start, long long& end) {
   const long long total = (long long)P.units * P.nc;
   start = (long long)t * P.w;
   if (start >= total) return 0;
-  end = min(start + (long long)P.w, total);
+  end = start + P.w < total ? start + P.w : total;
   const int us = (int)(start / P.nc), cs = (int)(start % P.nc);
   const int ue = (int)(end / P.nc), ce = (int)(end % P.nc);
   return (ce != 0) + (ue - (cs ? us + 1 : us)) + (cs != 0);
 }
 
-__device__ __forceinline__ WorkItem balance_item(const Balance& P, int N, int t, int k, long long start,
-                                                 long long end) {
+__host__ __device__ __forceinline__ WorkItem balance_item(const Balance& P, int N, int t, int k, long long start,
+                                                          long long end) {
   const int us = (int)(start / P.nc), cs = (int)(start % P.nc);
   const int ue = (int)(end / P.nc), ce = (int)(end % P.nc);
   const int f0 = cs ? us + 1 : us;
