@@ -182,8 +182,10 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   };
   auto item_chunks = [&](const WorkItem& w) { return w.hi > w.lo ? (w.hi - w.lo + kC - 1) / kC : 0; };
   // debug trace of one CTA: (bh = trace[15 * 4096], dv tile 0, segment 0); trace[15 * 4096] is set by the host
-  const bool tracing = trace != nullptr && !BAL && blockIdx.x == 0 && blockIdx.z == 0 &&
-                       blockIdx.y == (unsigned)trace[15 * 4096];
+  // (balanced launches: the CTA whose ticket is trace[15 * 4096]; events indexed by global chunk)
+  const bool tracing = trace != nullptr &&
+                       (BAL ? wl[0] == (int)trace[15 * 4096]
+                            : blockIdx.x == 0 && blockIdx.z == 0 && blockIdx.y == (unsigned)trace[15 * 4096]);
   const int lin_block = blockIdx.y * gridDim.x + blockIdx.x;
   auto gtime = [] {
     unsigned long long t;
@@ -291,7 +293,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       }
       fence_proxy_async_smem();
       tc_fence_before();
-      if (tracing && lane == 0) trace[(warp < 2 ? 3 : 4) * 4096 + c] = clock64();
+      if (tracing && lane == 0 && gc < 4096) trace[(warp < 2 ? 3 : 4) * 4096 + gc] = clock64();
       mbar_arrive(&epi1_bar[s]);
      }
     }
@@ -403,12 +405,12 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         }
         tc_fence_before();
         mbar_arrive(ds_free);
-        if (tracing && lane == 0 && sub == 0 && g == 0) trace[6 * 4096 + c] = clock64();
+        if (tracing && lane == 0 && sub == 0 && g == 0 && gc < 4096) trace[6 * 4096 + gc] = clock64();
         if (state_only) continue;
         if (c != nch - 1) {
           // buffer (gc+1)&1 was last read by Ox_{gc-1}, which precedes dS_gc in the tensor pipe
           publish((gc + 1) & 1);
-          if (tracing && lane == 0 && sub == 0 && g == 0) trace[7 * 4096 + c] = clock64();
+          if (tracing && lane == 0 && sub == 0 && g == 0 && gc < 4096) trace[7 * 4096 + gc] = clock64();
         }
         mbar_wait(&mma_o_bar[b], (gc >> 1) & 1);   // O_gc done
         tc_fence_after();
@@ -454,7 +456,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
           tma_store_3d(&tm_o, ot + kC * 128, w.j0 + 64, w.lo + c * kC, w.bh);
           bulk_commit();
         }
-        if (tracing && lane == 0 && sub == 0 && g == 0) trace[5 * 4096 + c] = clock64();
+        if (tracing && lane == 0 && sub == 0 && g == 0 && gc < 4096) trace[5 * 4096 + gc] = clock64();
       }
       LA_WRITE_STATE();
     }
@@ -472,7 +474,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
             const int s = gc % STAGES;
             const int t0 = w.lo + c * kC;
             mbar_wait(&empty[s], ((gc / STAGES) & 1) ^ 1);
-            if (tracing) trace[13 * 4096 + c] = clock64();
+            if (tracing && gc < 4096) trace[13 * 4096 + gc] = clock64();
             uint8_t* st = smem + s * G::STAGE_BYTES;
             mbar_arrive_expect_tx(&full[s], bytes);
 #pragma unroll
@@ -502,7 +504,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       auto issue_mma1 = [&](int c) {
         const int s = c % STAGES;
         mbar_wait(&full[s], (c / STAGES) & 1);
-        if (tracing && lane == 0) trace[10 * 4096 + c] = clock64();
+        if (tracing && lane == 0 && c < 4096) trace[10 * 4096 + c] = clock64();
         tc_fence_after();
         const uint64_t dq = dq0 + s * kStage, dk = dq + kQ;
 #pragma unroll
@@ -512,7 +514,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
             mma_bf16_ss_elect(tbase + T_P, dk + (kb * 512 + kk * 2), dq + (kb * 512 + kk * 2), id_qk,
                               (kb | kk) != 0);
         mma_commit_elect(mma1_bar);
-        if (tracing && lane == 0) trace[11 * 4096 + c] = clock64();
+        if (tracing && lane == 0 && c < 4096) trace[11 * 4096 + c] = clock64();
       };
       // the tensor pipe sees one flat chunk stream across the work list (c counts every chunk)
       int nchunks = 0;
@@ -526,24 +528,24 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         const uint64_t dk_mn = dmn0 + s * kStage + kQ;        // K', MN-major (B of V^T K')
         if (state_only) mbar_wait(&full[s], (c / STAGES) & 1);
         mbar_wait(&epi1_bar[s], (c / STAGES) & 1);     // P^T_c in smem (TMEM copy free), K'_c scaled
-        if (tracing && lane == 0) trace[12 * 4096 + c] = clock64();
+        if (tracing && lane == 0 && c < 4096) trace[12 * 4096 + c] = clock64();
         // P^T TMEM is free again: start MMA1 of the next chunk before this chunk's dS, so its
         // mask epilogue overlaps the state chain instead of following it
         if (!state_only && c + 1 < nchunks) issue_mma1(c + 1);
         if (c > 0) mbar_wait(ds_free, (c - 1) & 1);    // state warps hold dS_{c-1}
         tc_fence_after();
-        if (tracing && lane == 0) trace[1 * 4096 + c] = clock64();
+        if (tracing && lane == 0 && c < 4096) trace[1 * 4096 + c] = clock64();
 #pragma unroll
         for (int ks = 0; ks < kC / 16; ++ks)
           mma_bf16_ss_elect(tbase + T_DS, dv_mn + ks * 128, dk_mn + ks * 128, id_vk, ks != 0);
         mma_commit_elect(mma_s_bar);
         if (!state_only) {
           mbar_wait(&st_full[b], (c >> 1) & 1);        // S_c (bf16) published in TMEM buffer b
-          if (tracing && lane == 0) trace[14 * 4096 + c] = clock64();
+          if (tracing && lane == 0 && c < 4096) trace[14 * 4096 + c] = clock64();
           if (c >= 2) mbar_wait(&o_free[b], ((c >> 1) - 1) & 1);
           if (c >= 1) mbar_wait(ox_free, (c - 1) & 1);
           tc_fence_after();
-          if (tracing && lane == 0) trace[2 * 4096 + c] = clock64();
+          if (tracing && lane == 0 && c < 4096) trace[2 * 4096 + c] = clock64();
           const uint64_t dpt = dpt0 + b * (G::PT_BYTES >> 4);
 #pragma unroll
           for (int ks = 0; ks < kC / 16; ++ks)
