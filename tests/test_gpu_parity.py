@@ -200,8 +200,9 @@ def test_decode_steps_vs_oracle(la):
     assert orc.max_rel_error(st.cpu().numpy(), ref_s) <= TOL_F32
 
 
-@pytest.mark.parametrize("dk,dv", [(3, 5), (64, 62), (128, 512)])
+@pytest.mark.parametrize("dk,dv", [(3, 5), (64, 62), (128, 512), (128, 128), (64, 96), (32, 100), (256, 512)])
 def test_decode_odd_shapes(la, dk, dv):
+    """Few (b, h) states: the columns are split over CTAs (ragged last slice included)."""
     from paper_2501_02573_b200 import ops
     rng = np.random.default_rng(4)
     B, H = 2, 2
