@@ -6,6 +6,8 @@
 // contiguous run in shared memory (16-byte vector loads, broadcast across the warp).
 // Tokens are staged TC at a time by cp.async one chunk ahead, and each token's o partials go to
 // a [TC][RRG][128] shared buffer that is reduced once per chunk -- two barriers per TC tokens.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace linattn {
@@ -79,6 +81,8 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
     cp_async_commit();
   };
   const int nchunks = (N + TC - 1) / TC;
+  float sig = 1.f, inv = 1.f;                                // lazy decay state (see token_loop)
+  const float ginv = g > 0.f ? 1.f / g : 0.f;
   if (nchunks > 0) stage(0, 0);
   for (int ci = 0; ci < nchunks; ++ci) {
     const int c0 = ci * TC, buf = ci & 1;
@@ -93,11 +97,24 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
     const T* qc = qs + (size_t)buf * TC * dk;
     const T* kc = ks + (size_t)buf * TC * dk;
     const T* vc = vs + (size_t)buf * TC * RDV;
-    for (int t = 0; t < nt; ++t) {
+    // Lazy decay (gamma > 0): keep T = S / sig with sig = gamma^(tokens since the last renorm), so
+    // S <- gamma S + k^T v becomes T += (k / sig) v and o = (q sig) . T: one FMA per state element
+    // for the update instead of an FMUL and an FMA.  T is renormalised (T <- sig T) before sig
+    // underflows; gamma == 0 keeps the direct form.
+    auto token_loop = [&](auto lazy_tag) {
+     constexpr bool LAZY = decltype(lazy_tag)::value;
+     for (int t = 0; t < nt; ++t) {
       float vv[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) vv[e] = 4 * cv + e < nj ? to_f32(vc[t * RDV + 4 * cv + e]) : 0.f;
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      float kscale = 1.f, qscale = 1.f;
+      if constexpr (LAZY) {
+        sig *= g;
+        inv *= ginv;
+        kscale = inv;
+        qscale = sig;
+      }
       const T* kt = kc + t * dk + row0;
       const T* qt = qc + t * dk + row0;
 #pragma unroll
@@ -117,16 +134,35 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
 #pragma unroll
         for (int u = 0; u < EV2; ++u) {
           const int r = r0 + u;
-          const float kr = to_f32(kb8[u]), qr = to_f32(qb8[u]);
+          const float kr = to_f32(kb8[u]) * kscale, qr = to_f32(qb8[u]) * qscale;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            S[r][e] = fmaf(g, S[r][e], kr * vv[e]);
+            if constexpr (LAZY) S[r][e] = fmaf(kr, vv[e], S[r][e]);
+            else S[r][e] = fmaf(g, S[r][e], kr * vv[e]);
             acc[e] = fmaf(qr, S[r][e], acc[e]);
           }
         }
       }
       *reinterpret_cast<float4*>(part + ((size_t)t * RRG + rg) * RDV + 4 * cv) =
           make_float4(acc[0], acc[1], acc[2], acc[3]);
+      if constexpr (LAZY) {
+        if (sig < 0x1p-30f) {                                // uniform: same gamma for the CTA
+#pragma unroll
+          for (int r = 0; r < RMAXR; ++r)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) S[r][e] *= sig;
+          sig = 1.f;
+          inv = 1.f;
+        }
+      }
+     }
+    };
+    // (fp32 inputs keep the direct form: the lazy variant spills there and measured slower)
+    if constexpr (sizeof(T) == 2) {
+      if (g > 0.f) token_loop(std::true_type{});
+      else token_loop(std::false_type{});
+    } else {
+      token_loop(std::false_type{});
     }
     __syncthreads();                                         // all partials of the chunk written
     for (int x = tid; x < nt * RDV; x += RNT) {
@@ -146,7 +182,7 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int i = row0 + r, j = 4 * cv + e;
-        if (r < nrows && j < nj) s_out[((size_t)bh * dk + i) * dv + j0 + j] = S[r][e];
+        if (r < nrows && j < nj) s_out[((size_t)bh * dk + i) * dv + j0 + j] = sig * S[r][e];
       }
   }
 }
