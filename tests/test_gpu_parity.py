@@ -485,3 +485,24 @@ def test_random_shapes_fuzz(la, seed):
         out = ops.prefill(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_in=dev(s0), s_out=s_out, kernel=kernel)
         assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= tol, (dt, B, H, N, dk, dv)
         assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= max(tol, 5e-3), (dt, B, H, N, dk, dv)
+
+
+def test_recurrent_lazy_renormalisation(la):
+    """bf16 row recurrence keeps T = S / gamma^t and renormalises before gamma^t underflows:
+    small gammas (renormalised every ~20-60 tokens) over a long sequence, with the end state."""
+    from paper_2501_02573_b200 import ops
+    gam = [0.3, 0.5, 0.7, 0.999]
+    b, c, v = (orc.bf16_round(x) for x in orc.gen_inputs(1, 4, 700, 128, 128, np.float32, 23))
+    ref, ref_s = orc.seeded_blocked_attn(b, c, v, gam, True, None, block=64)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    s_out = torch.empty(1, 4, 128, 128, device="cuda")
+    out = ops.recurrent(dev(b, torch.bfloat16), dev(c, torch.bfloat16), dev(v, torch.bfloat16), l2, s_out=s_out)
+    assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
+    err_lazy = orc.max_rel_error(s_out.cpu().numpy(), ref_s)          # fp32 state from bf16 inputs
+    # the same values as fp32 inputs run the direct form (S <- gamma S + k^T v): the lazy form's
+    # state is as accurate (both at the fp32 1e-4 bar; accumulation error of 700 rank-1 updates)
+    s32 = torch.empty_like(s_out)
+    ops.recurrent(dev(b), dev(c), dev(v), l2, s_out=s32)
+    err_direct = orc.max_rel_error(s32.cpu().numpy(), ref_s)
+    assert err_lazy <= TOL_F32 and err_direct <= TOL_F32
+    assert err_lazy <= 4 * err_direct + 1e-6, (err_lazy, err_direct)
