@@ -138,6 +138,19 @@ def _pieces(batch: int, heads: int, target: int = 16):
     return [(slice(b, b + 1), slice(edges[i], edges[i + 1])) for b in range(batch) for i in range(per_b)]
 
 
+_STAGING: dict = {}   # (dtype, slot, role) -> pinned host buffer, grown on demand, kept across calls
+
+
+def _staging(dtype, slot: int, role: int, numel: int) -> torch.Tensor:
+    """A pinned host buffer of at least ``numel`` elements (cached: page-locking is slow)."""
+    key = (dtype, slot, role)
+    buf = _STAGING.get(key)
+    if buf is None or buf.numel() < numel:
+        buf = torch.empty(numel, dtype=dtype).pin_memory()
+        _STAGING[key] = buf
+    return buf[:numel]
+
+
 def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
     """Host tensors through the device in pieces: H2D(i+1) | prefill(i) | D2H(i-1) overlap.
 
@@ -145,7 +158,14 @@ def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
     pieces on the batch axis (or the head axis when B == 1) and each piece runs on three
     streams -- copy-in, compute (torch's current stream), copy-out -- ordered by events.
     With pinned host buffers both PCIe directions and the kernel run concurrently.
+
+    Pageable sources (numpy arrays, the reference's own calling convention) go through a
+    two-slot ring of pinned staging buffers in the COMPUTE dtype: the host copy into slot i%2
+    (multi-threaded, converting f64/f32 -> compute dtype on the way, so fewer bytes cross PCIe)
+    overlaps the DMA of the other slot; results come back in the compute dtype and are widened
+    while they are copied out of their pinned slot.
     """
+    numpy_in = not isinstance(inputs.v, torch.Tensor)
     b, c, v = (torch.from_numpy(np.ascontiguousarray(x)) if not isinstance(x, torch.Tensor) else x
                for x in (inputs.b, inputs.c, inputs.v))
     in_dtype = v.dtype
@@ -156,30 +176,59 @@ def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
     od = torch.empty(v.shape, dtype=cdt, device=dev)
     if result is None:
         result = torch.empty(v.shape, dtype=in_dtype)
+    elif not isinstance(result, torch.Tensor):
+        result = torch.from_numpy(result)
+    staged_in = not all(x.is_pinned() for x in (b, c, v))
+    staged_out = not result.is_pinned()
     log2g = ops.log2_gamma(inputs.gamma, inputs.decay, device=dev)
     compute = torch.cuda.current_stream(dev)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     s_in.wait_stream(compute)          # device buffers were allocated on the compute stream
-    for bs, hs in _pieces(v.shape[0], v.shape[1]):
+    slot_loaded = [None, None]         # H2D of the piece last staged in each slot
+    pending = None                     # (event, pinned slice, result view) still to copy out
+    for i, (bs, hs) in enumerate(_pieces(v.shape[0], v.shape[1])):
+        slot = i % 2
         loaded = torch.cuda.Event()
+        if staged_in and slot_loaded[slot] is not None:
+            slot_loaded[slot].synchronize()                # its previous DMA has read the slot
         with torch.cuda.stream(s_in):
-            for host, d in ((b, qd), (c, kd), (v, vd)):
+            for role, (host, d) in enumerate(((b, qd), (c, kd), (v, vd))):
                 src = host[bs, hs]
-                if src.dtype == cdt:
+                if staged_in:
+                    stg = _staging(cdt, slot, role, src.numel()).view(src.shape)
+                    stg.copy_(src)                           # host copy + cast, all cores
+                    d[bs, hs].copy_(stg, non_blocking=True)
+                elif src.dtype == cdt:
                     d[bs, hs].copy_(src, non_blocking=True)
-                else:   # stage in the host dtype, cast on the device
+                else:   # pinned, other dtype: stage in the host dtype, cast on the device
                     d[bs, hs].copy_(src.to(device=dev, non_blocking=True))
             loaded.record(s_in)
+        slot_loaded[slot] = loaded
         compute.wait_event(loaded)
         ops.prefill(qd[bs, hs], kd[bs, hs], vd[bs, hs], log2g[hs], out=od[bs, hs], kernel=kernel)
         computed = torch.cuda.Event()
         computed.record(compute)
+        done = torch.cuda.Event()
         with torch.cuda.stream(s_out):
             s_out.wait_event(computed)
-            src = od[bs, hs] if in_dtype == cdt else od[bs, hs].to(in_dtype)
-            result[bs, hs].copy_(src, non_blocking=result.is_pinned())
+            if staged_out:
+                ostg = _staging(cdt, slot, 3, od[bs, hs].numel()).view(od[bs, hs].shape)
+                ostg.copy_(od[bs, hs], non_blocking=True)
+            else:
+                src = od[bs, hs] if in_dtype == cdt else od[bs, hs].to(in_dtype)
+                result[bs, hs].copy_(src, non_blocking=True)
+            done.record(s_out)
+        if pending is not None:                            # previous piece: widen into result
+            pending[0].synchronize()
+            pending[2].copy_(pending[1])
+            pending = None
+        if staged_out:
+            pending = (done, ostg, result[bs, hs])
+    if pending is not None:
+        pending[0].synchronize()
+        pending[2].copy_(pending[1])
     s_out.synchronize()
-    return result
+    return result.numpy() if numpy_in else result
 
 
 def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None = None,
@@ -202,7 +251,7 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
     host = not inputs.on_device
     torch_host = inputs.on_device and not inputs.v.is_cuda
     in_dtype = inputs.v.dtype
-    if torch_host and method in (MethodId.B200_CHUNKED, MethodId.B200_CHUNKED_F32):
+    if (torch_host or host) and method in (MethodId.B200_CHUNKED, MethodId.B200_CHUNKED_F32):
         if not torch.cuda.is_available():
             raise LinAttnError("no CUDA device: the B200 path has no CPU fallback")
         kernel = "auto" if method is MethodId.B200_CHUNKED else "simt"
