@@ -435,6 +435,25 @@ def run_ours(args):
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
     del qh, kh, vh, oh, inputs
 
+    # the reference's own calling convention: pageable numpy f32 arrays (make_inputs), the method
+    # auto resolves to for f32 (the fp32 parity route), validate=False as in the reference bench
+    e2e_np = None
+    if not args.no_extra:
+        npin = [x.float().cpu().numpy() for x in (q, k, v)]
+        inputs = la.make_inputs(*npin, gamma=gam, decay=True)
+        meth = la.default_policy().resolve(B, N, True, "f32")[0]
+        la.run_method(meth, inputs, validate=False)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            la.run_method(meth, inputs, validate=False)
+        torch.cuda.synchronize()
+        np_s = max_over_ranks((time.perf_counter() - t0) / 3)
+        e2e_np = {"value": world * tokens_per_rank / np_s, "unit": "tokens/s", "ms_per_step": np_s * 1e3,
+                  "h2d_bytes_per_step": 3 * B * H * N * dk * 4, "d2h_bytes_per_step": B * H * N * dv * 4,
+                  "api": f"run_method({meth.value}) on pageable numpy f32 arrays (pinned staging inside)"}
+        del npin, inputs
+
     # decode step (configs[3]): 1024 single-token steps, state 256x32x128x128 fp32 (512 MiB)
     dec = None
     if not args.no_decode:
@@ -485,6 +504,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": 3 * B * H * N * dk * 2, "d2h_bytes_per_step": B * H * N * dv * 2,
                 "ms_per_step": e2e_s * 1e3,
                 "api": "run_method(b200-chunked) on pinned host bf16 tensors (H2D | kernel | D2H overlapped per batch piece)"},
+        "e2e_numpy_f32": e2e_np,
         "gpu_launches": int(max_over_ranks(launches)),
         "clocks": clk.summary(),
         "decode": dec,
