@@ -27,6 +27,7 @@ There is no CPU fallback: without the CUDA library every method raises.
 from __future__ import annotations
 
 import enum
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -95,13 +96,19 @@ _COMPUTE = {
 }
 
 
-def _to_device(x, dtype):
-    if isinstance(x, torch.Tensor):
-        if x.is_cuda:
-            return x.to(dtype=dtype).contiguous()
-        # host torch tensor: async H2D when pinned, then cast on the device
-        return x.to(device="cuda", non_blocking=x.is_pinned()).to(dtype=dtype).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(x)).to(device="cuda").to(dtype=dtype)
+def _to_device(x, dtype, role: int = 0):
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        return x.to(dtype=dtype).contiguous()
+    if isinstance(x, torch.Tensor) and x.is_pinned():
+        # pinned host tensor: async H2D, then cast on the device
+        return x.to(device="cuda", non_blocking=True).to(dtype=dtype).contiguous()
+    # pageable (numpy or torch): cast on the host into a pinned staging buffer, then DMA
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    stg = _staging(dtype, 2, 10 + role, t.numel()).view(t.shape)
+    stg.copy_(t)
+    d = stg.to(device="cuda", non_blocking=True)
+    torch.cuda.current_stream().synchronize()         # the staging buffer is reused by the next call
+    return d
 
 
 def _seqpar(q, k, v, log2g, parts: int, kernel: str):
@@ -138,16 +145,22 @@ def _pieces(batch: int, heads: int, target: int = 16):
     return [(slice(b, b + 1), slice(edges[i], edges[i + 1])) for b in range(batch) for i in range(per_b)]
 
 
-_STAGING: dict = {}   # (dtype, slot, role) -> pinned host buffer, grown on demand, kept across calls
+# (dtype, slot, role) -> pinned host buffer, grown on demand and kept across calls (page-locking
+# is slow); per thread, so concurrent run_method calls never share a staging buffer (the
+# reference's calls are reentrant)
+_STAGING = threading.local()
 
 
 def _staging(dtype, slot: int, role: int, numel: int) -> torch.Tensor:
-    """A pinned host buffer of at least ``numel`` elements (cached: page-locking is slow)."""
+    """A pinned host buffer of at least ``numel`` elements, private to the calling thread."""
+    cache = getattr(_STAGING, "bufs", None)
+    if cache is None:
+        cache = _STAGING.bufs = {}
     key = (dtype, slot, role)
-    buf = _STAGING.get(key)
+    buf = cache.get(key)
     if buf is None or buf.numel() < numel:
         buf = torch.empty(numel, dtype=dtype).pin_memory()
-        _STAGING[key] = buf
+        cache[key] = buf
     return buf[:numel]
 
 
@@ -259,9 +272,9 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
         chunk = TC_CHUNK if method is MethodId.B200_CHUNKED else SIMT_CHUNK
         return res, ops.chunked_opcount(inputs.batch, inputs.heads, inputs.seqlen, inputs.rank,
                                         inputs.dim, inputs.decay, chunk)
-    q = _to_device(inputs.b, cdt)
-    k = _to_device(inputs.c, cdt)
-    v = _to_device(inputs.v, cdt)
+    q = _to_device(inputs.b, cdt, 0)
+    k = _to_device(inputs.c, cdt, 1)
+    v = _to_device(inputs.v, cdt, 2)
     log2g = ops.log2_gamma(inputs.gamma, inputs.decay, device=q.device)
     if method is MethodId.B200_CHUNKED:
         out_dev = ops.prefill(q, k, v, log2g, kernel="auto")
@@ -282,7 +295,11 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
             3 if inputs.decay else 2)  # reference row-based count (kernels.py:105)
     result = out
     if host:
-        res = out_dev.float().cpu().numpy().astype(in_dtype, copy=False)
+        # D2H through a pinned staging buffer (pageable D2H is several times slower), then widen
+        stg = _staging(out_dev.dtype, 2, 20, out_dev.numel()).view(out_dev.shape)
+        stg.copy_(out_dev, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        res = (stg.float() if stg.dtype == torch.bfloat16 else stg).numpy().astype(in_dtype)
         if result is not None:
             result[...] = res
             return result, ops_count
