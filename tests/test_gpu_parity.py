@@ -506,3 +506,36 @@ def test_recurrent_lazy_renormalisation(la):
     err_direct = orc.max_rel_error(s32.cpu().numpy(), ref_s)
     assert err_lazy <= TOL_F32 and err_direct <= TOL_F32
     assert err_lazy <= 4 * err_direct + 1e-6, (err_lazy, err_direct)
+
+
+def test_numpy_inputs_concurrent_threads(la):
+    """The reference's calling convention (pageable numpy) from two host threads at once: the
+    pinned staging buffers are per thread, so results equal the serial ones bitwise."""
+    import threading
+    rng = np.random.default_rng(9)
+    cases = []
+    for (B, H, N, d) in [(2, 3, 700, 64), (3, 2, 1300, 128)]:
+        b, c, v = (rng.standard_normal((B, H, N, d)).astype(np.float32) for _ in range(3))
+        cases.append(la.make_inputs(b, c, v, gamma=[0.9] * H, decay=True))
+    methods = ["b200-chunked", "b200-chunked-f32", "b200-recurrent"]
+    serial = {(i, m): la.run_method(la.MethodId.parse(m), inp)[0] for i, inp in enumerate(cases) for m in methods}
+    got, errors = {}, []
+
+    def worker(order):
+        try:
+            for rep in range(2):
+                for i in order:
+                    for m in methods:
+                        got[(threading.get_ident(), rep, i, m)] = la.run_method(la.MethodId.parse(m), cases[i])[0]
+        except Exception as e:   # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(o,)) for o in ([0, 1], [1, 0])]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for (_, _, i, m), out in got.items():
+        assert isinstance(out, np.ndarray) and out.dtype == np.float32
+        np.testing.assert_array_equal(out, serial[(i, m)])
