@@ -15,6 +15,9 @@ namespace {
 constexpr int CH = 32;    // chunk length
 constexpr int DVT = 64;   // dv columns per CTA
 constexpr int NT = 256;   // threads per CTA
+#ifndef SIMT_O44
+#define SIMT_O44 1        // 4x4 output tiles with the dk reduction split in halves (0: 2x4 tiles)
+#endif
 
 template <typename T>
 __global__ void __launch_bounds__(NT)
@@ -169,6 +172,7 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
   float* S = A + CH * (CH + 4);               // [dk][DVT]
   float* w = S + (size_t)dk * DVT;            // [CH] gamma^(L-1-s)
   float* gq = w + CH;                         // [CH] gamma^(t+1)
+  float* red = gq + CH;                       // SIMT_O44: [128][16] partial outputs of the k halves
   constexpr int LA = CH + 4;
 
   const int tid = threadIdx.x;
@@ -317,6 +321,70 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
       }
       __syncthreads();
       // O_t = A_t V + gamma^(t+1) q_t S   (rows tO, tO+1; columns jO..jO+3)
+#if SIMT_O44
+      {
+        // 4 x 4 output tiles over 128 threads per half: each half reduces half of dk (and of
+        // the intra sources), one float4 of Q / A per row feeds 16 FMAs, halves summed in smem
+        const int kh = tid >> 7, tt = tid & 127;
+        const int r0 = 4 * (tt >> 4), jq = 4 * (tt & 15);
+        float in[4][4], ex[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) in[r][e] = ex[r][e] = 0.f;
+        auto step4 = [](float (&acc)[4], const float4 a, const float4& b0, const float4& b1,
+                        const float4& b2, const float4& b3) {
+          acc[0] = fmaf(a.x, b0.x, fmaf(a.y, b1.x, fmaf(a.z, b2.x, fmaf(a.w, b3.x, acc[0]))));
+          acc[1] = fmaf(a.x, b0.y, fmaf(a.y, b1.y, fmaf(a.z, b2.y, fmaf(a.w, b3.y, acc[1]))));
+          acc[2] = fmaf(a.x, b0.z, fmaf(a.y, b1.z, fmaf(a.z, b2.z, fmaf(a.w, b3.z, acc[2]))));
+          acc[3] = fmaf(a.x, b0.w, fmaf(a.y, b1.w, fmaf(a.z, b2.w, fmaf(a.w, b3.w, acc[3]))));
+        };
+        const int sc_lo = kh * (CH / 2), sc_hi = min(sc_lo + CH / 2, r0 + 4);
+        for (int sc = sc_lo; sc < sc_hi; sc += 4) {
+          const float4 v0 = *reinterpret_cast<const float4*>(Vc + (sc + 0) * DVT + jq);
+          const float4 v1 = *reinterpret_cast<const float4*>(Vc + (sc + 1) * DVT + jq);
+          const float4 v2 = *reinterpret_cast<const float4*>(Vc + (sc + 2) * DVT + jq);
+          const float4 v3 = *reinterpret_cast<const float4*>(Vc + (sc + 3) * DVT + jq);
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            step4(in[r], *reinterpret_cast<const float4*>(A + (r0 + r) * LA + sc), v0, v1, v2, v3);
+        }
+        const int k_lo = kh * (dk / 2);
+        for (int i = k_lo; i < k_lo + dk / 2; i += 4) {
+          const float4 s0 = *reinterpret_cast<const float4*>(S + (i + 0) * DVT + jq);
+          const float4 s1 = *reinterpret_cast<const float4*>(S + (i + 1) * DVT + jq);
+          const float4 s2 = *reinterpret_cast<const float4*>(S + (i + 2) * DVT + jq);
+          const float4 s3 = *reinterpret_cast<const float4*>(S + (i + 3) * DVT + jq);
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            step4(ex[r], *reinterpret_cast<const float4*>(Qs + (r0 + r) * ld + i), s0, s1, s2, s3);
+        }
+        float4* rd = reinterpret_cast<float4*>(red) + tt * 4;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float g = gq[r0 + r];
+          const float4 o4 = make_float4(fmaf(g, ex[r][0], in[r][0]), fmaf(g, ex[r][1], in[r][1]),
+                                        fmaf(g, ex[r][2], in[r][2]), fmaf(g, ex[r][3], in[r][3]));
+          if (kh == 1) rd[r] = o4;
+          else {
+            in[r][0] = o4.x; in[r][1] = o4.y; in[r][2] = o4.z; in[r][3] = o4.w;
+          }
+        }
+        __syncthreads();
+        if (kh == 0) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int t = r0 + r;
+            if (t >= L) continue;
+            const float4 p = rd[r];
+            const float ov[4] = {in[r][0] + p.x, in[r][1] + p.y, in[r][2] + p.z, in[r][3] + p.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (jq + e < nj) ob[(size_t)(c0 + t) * dv + j0 + jq + e] = from_f32<T>(ov[e]);
+          }
+        }
+      }
+#else
       {
         float in0[4] = {0.f, 0.f, 0.f, 0.f}, in1[4] = {0.f, 0.f, 0.f, 0.f};
         float ex0[4] = {0.f, 0.f, 0.f, 0.f}, ex1[4] = {0.f, 0.f, 0.f, 0.f};
@@ -360,6 +428,7 @@ prefill_simt_rb_kernel(const T* __restrict__ q, const T* __restrict__ k, const T
             if (jO + e < nj) ob[(size_t)(c0 + t) * dv + j0 + jO + e] = from_f32<T>(in[e] + g * ex[e]);
         }
       }
+#endif
       __syncthreads();   // Q.S reads of S done before the update below
       if constexpr (ASYNC) {
         // every read of Q for this chunk is done: stream the next chunk's Q in behind the update
@@ -433,7 +502,7 @@ int rb_mode(const void* q, const void* k, const void* v, const ShapeArgs& s, int
                         reinterpret_cast<uintptr_t>(q)) & 15);
   for (int nb = async ? 2 : 1; nb >= 1; --nb) {
     smem = sizeof(float) * ((1 + nb) * CH * ((size_t)s.dk + 4) + nb * CH * DVT + CH * (CH + 4) +
-                            (size_t)s.dk * DVT + 2 * CH);
+                            (size_t)s.dk * DVT + 2 * CH + (SIMT_O44 ? 128 * 16 : 0));
     if (smem <= 227 * 1024) return nb == 2 ? 2 : 1;
   }
   return 0;
