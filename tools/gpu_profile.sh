@@ -15,6 +15,8 @@ full cfg2_prefill prefill_tc_pipe 2 PROF_SHAPE=8,32,8192,128
 full cfg3_prefill tmem_state 2 PROF_SHAPE=4,16,16384,256,512
 full cfg5_statepass prefill_tc_pipe 4 PROF_SHAPE=1,32,131072,128
 full cfg5_prefill prefill_tc_pipe 5 PROF_SHAPE=1,32,131072,128
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:simt -s 1 -c 1 \
+    -o $OUT/prof_fp32_prefill_$TAG python tools/f32_once.py > $OUT/prof_fp32_prefill_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_step -s 5 -c 1 \
     -o $OUT/prof_decode_$TAG python bench.py --steps 1 --warmup 3 --no-cpu --no-extra --decode-steps 64 \
     > $OUT/prof_decode_$TAG.log 2>&1
