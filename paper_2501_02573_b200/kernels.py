@@ -96,19 +96,9 @@ _COMPUTE = {
 }
 
 
-def _to_device(x, dtype, role: int = 0):
-    if isinstance(x, torch.Tensor) and x.is_cuda:
-        return x.to(dtype=dtype).contiguous()
-    if isinstance(x, torch.Tensor) and x.is_pinned():
-        # pinned host tensor: async H2D, then cast on the device
-        return x.to(device="cuda", non_blocking=True).to(dtype=dtype).contiguous()
-    # pageable (numpy or torch): cast on the host into a pinned staging buffer, then DMA
-    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
-    stg = _staging(dtype, 2, 10 + role, t.numel()).view(t.shape)
-    stg.copy_(t)
-    d = stg.to(device="cuda", non_blocking=True)
-    torch.cuda.current_stream().synchronize()         # the staging buffer is reused by the next call
-    return d
+def _to_device(x, dtype):
+    """Device (CUDA) tensors only: host inputs go through ``_host_pipelined``."""
+    return x.to(dtype=dtype).contiguous()
 
 
 def _seqpar(q, k, v, log2g, parts: int, kernel: str):
@@ -164,7 +154,7 @@ def _staging(dtype, slot: int, role: int, numel: int) -> torch.Tensor:
     return buf[:numel]
 
 
-def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
+def _host_pipelined(inputs: AttnInputs, cdt, run, result, pieces: int = 16):
     """Host tensors through the device in pieces: H2D(i+1) | prefill(i) | D2H(i-1) overlap.
 
     Every (batch, head) slice is independent (kernels.py:273-280), so the batch is cut into
@@ -199,7 +189,7 @@ def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
     s_in.wait_stream(compute)          # device buffers were allocated on the compute stream
     slot_loaded = [None, None]         # H2D of the piece last staged in each slot
     pending = None                     # (event, pinned slice, result view) still to copy out
-    for i, (bs, hs) in enumerate(_pieces(v.shape[0], v.shape[1])):
+    for i, (bs, hs) in enumerate(_pieces(v.shape[0], v.shape[1], pieces)):
         slot = i % 2
         loaded = torch.cuda.Event()
         if staged_in and slot_loaded[slot] is not None:
@@ -218,7 +208,7 @@ def _host_pipelined(inputs: AttnInputs, cdt, kernel: str, result):
             loaded.record(s_in)
         slot_loaded[slot] = loaded
         compute.wait_event(loaded)
-        ops.prefill(qd[bs, hs], kd[bs, hs], vd[bs, hs], log2g[hs], out=od[bs, hs], kernel=kernel)
+        run(qd[bs, hs], kd[bs, hs], vd[bs, hs], log2g[hs], od[bs, hs])
         computed = torch.cuda.Event()
         computed.record(compute)
         done = torch.cuda.Event()
@@ -264,17 +254,32 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
     host = not inputs.on_device
     torch_host = inputs.on_device and not inputs.v.is_cuda
     in_dtype = inputs.v.dtype
-    if (torch_host or host) and method in (MethodId.B200_CHUNKED, MethodId.B200_CHUNKED_F32):
+    if torch_host or host:
+        # host tensors: (batch, head) pieces through the overlapped copy/compute pipeline
         if not torch.cuda.is_available():
             raise LinAttnError("no CUDA device: the B200 path has no CPU fallback")
-        kernel = "auto" if method is MethodId.B200_CHUNKED else "simt"
-        res = _host_pipelined(inputs, cdt, kernel, out)
-        chunk = TC_CHUNK if method is MethodId.B200_CHUNKED else SIMT_CHUNK
-        return res, ops.chunked_opcount(inputs.batch, inputs.heads, inputs.seqlen, inputs.rank,
-                                        inputs.dim, inputs.decay, chunk)
-    q = _to_device(inputs.b, cdt, 0)
-    k = _to_device(inputs.c, cdt, 1)
-    v = _to_device(inputs.v, cdt, 2)
+        if method is MethodId.B200_RECURRENT:
+            def run(q, k, v, l2, o):
+                ev = 16 // q.element_size()
+                if q.shape[3] % ev == 0 and v.shape[3] % ev == 0 and q.shape[3] <= 256:
+                    ops.recurrent(q, k, v, l2, out=o)
+                else:
+                    o.copy_(_recurrent(q, k, v, l2))
+            ops_count = inputs.batch * inputs.heads * inputs.seqlen * inputs.rank * inputs.dim * (
+                3 if inputs.decay else 2)  # reference row-based count (kernels.py:105)
+        else:
+            kernel = "simt" if method is MethodId.B200_CHUNKED_F32 else "auto"
+            split = max(1, int(params.seq_parts)) if method is MethodId.B200_SEQPAR else None
+            run = lambda q, k, v, l2, o: ops.prefill(q, k, v, l2, out=o, kernel=kernel, seq_split=split)  # noqa: E731
+            chunk = SIMT_CHUNK if method is MethodId.B200_CHUNKED_F32 else TC_CHUNK
+            ops_count = ops.chunked_opcount(inputs.batch, inputs.heads, inputs.seqlen, inputs.rank,
+                                            inputs.dim, inputs.decay, chunk)
+        # the row recurrence is one serial chain per (b, h): few, wide pieces keep the SMs busy
+        pieces = 2 if method is MethodId.B200_RECURRENT else 16
+        return _host_pipelined(inputs, cdt, run, out, pieces), ops_count
+    q = _to_device(inputs.b, cdt)
+    k = _to_device(inputs.c, cdt)
+    v = _to_device(inputs.v, cdt)
     log2g = ops.log2_gamma(inputs.gamma, inputs.decay, device=q.device)
     if method is MethodId.B200_CHUNKED:
         out_dev = ops.prefill(q, k, v, log2g, kernel="auto")
@@ -293,25 +298,7 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
     if method is MethodId.B200_RECURRENT:
         ops_count = inputs.batch * inputs.heads * inputs.seqlen * inputs.rank * inputs.dim * (
             3 if inputs.decay else 2)  # reference row-based count (kernels.py:105)
-    result = out
-    if host:
-        # D2H through a pinned staging buffer (pageable D2H is several times slower), then widen
-        stg = _staging(out_dev.dtype, 2, 20, out_dev.numel()).view(out_dev.shape)
-        stg.copy_(out_dev, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        res = (stg.float() if stg.dtype == torch.bfloat16 else stg).numpy().astype(in_dtype)
-        if result is not None:
-            result[...] = res
-            return result, ops_count
-        return res, ops_count
-    out = out_dev
-    if torch_host:
-        if result is None:
-            return out.to(in_dtype).cpu(), ops_count
-        result.copy_(out.to(in_dtype), non_blocking=result.is_pinned())
-        torch.cuda.current_stream().synchronize()
-        return result, ops_count
-    if result is not None:
-        result.copy_(out)
-        return result, ops_count
-    return out.to(in_dtype), ops_count
+    if out is not None:
+        out.copy_(out_dev)
+        return out, ops_count
+    return out_dev.to(in_dtype), ops_count
