@@ -45,7 +45,7 @@ static int check_dims(const ShapeArgs& s, bool need_n) {
   if (s.dv < 1) return fail(LINATTN_ESHAPE, "dim extent must be >= 1, got %lld", (long long)s.dv);
   if (s.N > (1LL << 31) - 1 || s.B * s.H > (1LL << 31) - 1)
     return fail(LINATTN_ESHAPE, "extent too large for 32-bit indexing");
-  if (need_n && s.B * s.H > 65535)   // sequence kernels put batch*heads on grid.y
+  if (need_n && s.B * s.H > 65535)   // sequence kernels put batch*heads on grid.y (ops.py splits the batch)
     return fail(LINATTN_EUNSUPPORTED, "batch*heads = %lld exceeds 65535 for one launch; split the batch",
                 (long long)(s.B * s.H));
   return LINATTN_OK;

@@ -69,6 +69,17 @@ def log2_gamma(gammas, decay: bool = True, device=None) -> torch.Tensor:
     return t.to(device) if device is not None else t
 
 
+_MAX_GRID_Y = 65535   # the sequence kernels put batch*heads on grid.y
+
+
+def _batch_chunks(B: int, H: int):
+    """Contiguous batch ranges with at most 65535 (batch, head) units each (one launch each)."""
+    if B * H <= _MAX_GRID_Y or H > _MAX_GRID_Y:
+        return [(0, B)]
+    step = _MAX_GRID_Y // H
+    return [(b0, min(B, b0 + step)) for b0 in range(0, B, step)]
+
+
 def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "auto",
             seq_split: int | None = None):
     """O = (Q K^T (.) M_gamma) V on device; optional initial/end state (fp32).
@@ -104,9 +115,11 @@ def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "a
         if st is not None and (st.dtype != torch.float32 or tuple(st.shape) != (B, H, dk, dv)):
             raise ShapeError(f"state must be float32 [B,H,dk,dv]={B, H, dk, dv}, got {tuple(st.shape)}")
     lib = _lib.load()
-    _lib.check(lib.linattn_prefill(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                                   log2g.data_ptr(), _ptr(s_in), _ptr(s_out), B, H, N, dk, dv,
-                                   _dtype_code(q), _KERNELS[kernel], _stream()))
+    for b0, b1 in _batch_chunks(B, H):   # more than 65535 (batch, head) units: one launch per chunk
+        sl = (lambda t: None if t is None else t[b0:b1])   # noqa: E731
+        _lib.check(lib.linattn_prefill(q[b0:b1].data_ptr(), k[b0:b1].data_ptr(), v[b0:b1].data_ptr(),
+                                       out[b0:b1].data_ptr(), log2g.data_ptr(), _ptr(sl(s_in)), _ptr(sl(s_out)),
+                                       b1 - b0, H, N, dk, dv, _dtype_code(q), _KERNELS[kernel], _stream()))
     return out
 
 
@@ -118,8 +131,10 @@ def state_pass(k, v, log2g, *, s_out=None, kernel: str = "auto"):
     if s_out is None:
         s_out = torch.empty((B, H, dk, dv), dtype=torch.float32, device=k.device)
     lib = _lib.load()
-    _lib.check(lib.linattn_state_pass(k.data_ptr(), v.data_ptr(), s_out.data_ptr(), log2g.data_ptr(),
-                                      B, H, N, dk, dv, _dtype_code(k), _KERNELS[kernel], _stream()))
+    for b0, b1 in _batch_chunks(B, H):
+        _lib.check(lib.linattn_state_pass(k[b0:b1].data_ptr(), v[b0:b1].data_ptr(), s_out[b0:b1].data_ptr(),
+                                          log2g.data_ptr(), b1 - b0, H, N, dk, dv, _dtype_code(k),
+                                          _KERNELS[kernel], _stream()))
     return s_out
 
 
@@ -238,8 +253,11 @@ def recurrent(q, k, v, log2g, *, s_in=None, s_out=None, out=None):
     if out is None:
         out = torch.empty_like(v)
     lib = _lib.load()
-    _lib.check(lib.linattn_recurrent(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), log2g.data_ptr(),
-                                     _ptr(s_in), _ptr(s_out), B, H, N, dk, dv, _dtype_code(q), _stream()))
+    for b0, b1 in _batch_chunks(B, H):
+        sl = (lambda t: None if t is None else t[b0:b1])   # noqa: E731
+        _lib.check(lib.linattn_recurrent(q[b0:b1].data_ptr(), k[b0:b1].data_ptr(), v[b0:b1].data_ptr(),
+                                         out[b0:b1].data_ptr(), log2g.data_ptr(), _ptr(sl(s_in)), _ptr(sl(s_out)),
+                                         b1 - b0, H, N, dk, dv, _dtype_code(q), _stream()))
     return out
 
 

@@ -247,3 +247,27 @@ def test_balanced_schedule_fp32(ops, B, H, N, dk, dv):
     out = ops.prefill(dev(b), dev(c), dev(v), l2, s_in=dev(s0), s_out=s_out, kernel="simt")
     assert orc.max_rel_error(out.cpu().numpy(), ref) <= TOL_F32
     assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= TOL_F32
+
+
+def test_batch_heads_beyond_grid_limit(ops):
+    """More than 65535 (batch, head) units: ops splits the batch into launches of <= 65535 units
+    (the C ABI rejects larger ones); results equal independent smaller calls bitwise."""
+    B, H, N, d = 2100, 32, 3, 16
+    g = torch.Generator(device="cuda").manual_seed(5)
+    l2 = ops.log2_gamma([0.5 + 0.015 * h for h in range(H)], True, "cuda")
+    for dt, kernel in ((torch.bfloat16, "auto"), (torch.float32, "simt")):
+        q, k, v = (torch.randn(B, H, N, d, device="cuda", dtype=dt, generator=g) for _ in range(3))
+        s0 = torch.randn(B, H, d, d, device="cuda", generator=g)
+        s_out = torch.empty_like(s0)
+        out = ops.prefill(q, k, v, l2, s_in=s0, s_out=s_out, kernel=kernel)
+        for b0, b1 in ((0, 1000), (1000, B)):
+            so = torch.empty_like(s0[b0:b1])
+            part = ops.prefill(q[b0:b1].contiguous(), k[b0:b1].contiguous(), v[b0:b1].contiguous(), l2,
+                               s_in=s0[b0:b1].contiguous(), s_out=so, kernel=kernel)
+            assert torch.equal(part, out[b0:b1]) and torch.equal(so, s_out[b0:b1])
+        rec = ops.recurrent(q, k, v, l2)
+        assert torch.equal(rec[1000:1010], ops.recurrent(q[1000:1010].contiguous(), k[1000:1010].contiguous(),
+                                                          v[1000:1010].contiguous(), l2))
+        ref = orc.oracle_attn(q[2099:].float().cpu().numpy(), k[2099:].float().cpu().numpy(),
+                              v[2099:].float().cpu().numpy(), [0.5 + 0.015 * h for h in range(H)], True)
+        assert orc.max_rel_error(rec[2099:].float().cpu().numpy(), ref) <= (TOL_F32 if dt == torch.float32 else TOL_BF16)
