@@ -260,11 +260,32 @@ int linattn_state_pass(const void* k, const void* v, float* s_out, const float* 
   const bool tc_ok = tc_supported(s, dtype) && aligned16({k, v});
   if (kernel == LINATTN_KERNEL_TC && !tc_ok)
     return fail(LINATTN_EUNSUPPORTED, "tensor-core state pass needs bf16, a supported shape and aligned tensors");
-  if (kernel != LINATTN_KERNEL_SIMT && tc_ok)
-    return cuda_status(launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, s_out, s, true,
-                                         SegArgs{}, 1, st), "state_pass_tc");
-  return cuda_status(launch_prefill_simt(nullptr, k, v, nullptr, log2g, nullptr, s_out, s, dtype,
-                                         true, SegArgs{}, 1, st), "state_pass_simt");
+  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_ok;
+  auto launch = [&](float* so, const SegArgs& a, int nz) {
+    return tc ? launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, so, s, true, a, nz, st)
+              : launch_prefill_simt(nullptr, k, v, nullptr, log2g, nullptr, so, s, dtype, true, a, nz, st);
+  };
+  // few (b, h) units: every segment's local state in parallel (the split plan of the prefill,
+  // all nseg segments here), then the end state = the state at N from them (one scan)
+  const Plan pl = plan_split(s, tc);
+  if (pl.nseg > 1) {
+    const int64_t nloc = pl.nseg * pl.m;
+    const size_t bytes = (size_t)nloc * s.B * s.H * s.dk * s.dv * sizeof(float);
+    float* loc = nullptr;
+    cudaMemPool_t pool = work_pool();
+    if (pool && cudaMallocFromPoolAsync((void**)&loc, bytes, pool, st) == cudaSuccess) {
+      cudaError_t e = launch(loc, make_seg(pl.seg_len, pl.m), (int)nloc);
+      if (e == cudaSuccess) {
+        SegArgs a = make_seg(s.N, 1);
+        attach_loc(a, loc, pl.seg_len, pl.m, nloc);
+        e = launch_state_at(loc, nullptr, s_out, a, s.N, log2g, s, st);
+      }
+      cudaFreeAsync(loc, st);
+      return cuda_status(e, tc ? "state_pass_tc (split)" : "state_pass_simt (split)");
+    }
+    cudaGetLastError();
+  }
+  return cuda_status(launch(s_out, SegArgs{}, 1), tc ? "state_pass_tc" : "state_pass_simt");
 }
 
 static int check_seg(const ShapeArgs& s, int64_t seg_len, int64_t m, bool tc) {

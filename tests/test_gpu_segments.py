@@ -271,3 +271,21 @@ def test_batch_heads_beyond_grid_limit(ops):
         ref = orc.oracle_attn(q[2099:].float().cpu().numpy(), k[2099:].float().cpu().numpy(),
                               v[2099:].float().cpu().numpy(), [0.5 + 0.015 * h for h in range(H)], True)
         assert orc.max_rel_error(rec[2099:].float().cpu().numpy(), ref) <= (TOL_F32 if dt == torch.float32 else TOL_BF16)
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
+def test_state_pass_split(ops, dt):
+    """Few (b, h) units: the state pass runs every segment in parallel and scans them (the same
+    plan as the prefill split); the end state matches the oracle and the unsplit prefill's s_out."""
+    gam = [0.0, 0.97, 1 - 2.0 ** -12]
+    b, c, v = orc.gen_inputs(1, 3, 5000, 128, 128, np.float32, 77)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    kernel = "auto" if dt == torch.bfloat16 else "simt"
+    assert ops.seq_plan(1, 3, 5000, 128, 128, dt, kernel)[1] > 1
+    s = ops.state_pass(dev(c, dt), dev(v, dt), l2, kernel=kernel)
+    ref = np.stack([[orc.segment_end_state(c[0, h], v[0, h], gam[h]) for h in range(3)]])
+    assert orc.max_rel_error(s.cpu().numpy(), ref) <= (2e-3 if dt == torch.bfloat16 else 1e-5)
+    s1 = torch.empty_like(s)
+    ops.prefill(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_out=s1, kernel=kernel, seq_split=1)
+    assert orc.max_rel_error(s.cpu().numpy(), s1.cpu().numpy()) <= (2e-3 if dt == torch.bfloat16 else 1e-5)
