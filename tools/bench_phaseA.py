@@ -1,5 +1,6 @@
+"""Dev timing of the split state pass (phase A) at the 8-GPU configs[4] slice, by sub-split m."""
 import os, sys, json
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2501_02573_b200 import ops
 B, H, N, d = 1, 32, 16384, 128
