@@ -141,6 +141,12 @@ def _pieces(batch: int, heads: int, target: int = 16):
 _STAGING = threading.local()
 
 
+def release_staging_buffers() -> None:
+    """Free the calling thread's cached pinned staging buffers (host-input ``run_method`` calls
+    keep up to eight piece-sized page-locked buffers per thread for reuse)."""
+    _STAGING.__dict__.pop("bufs", None)
+
+
 def _staging(dtype, slot: int, role: int, numel: int) -> torch.Tensor:
     """A pinned host buffer of at least ``numel`` elements, private to the calling thread."""
     cache = getattr(_STAGING, "bufs", None)

@@ -217,3 +217,9 @@ def test_bench_render_and_usage_errors():
         run_bench(BenchConfig(methods=[MethodId.AUTO], grid=[(1, 1, 8, 2, 2)]))
     with pytest.raises(UsageError):
         run_bench(BenchConfig(methods=[MethodId.B200_CHUNKED], grid=[]))
+
+
+def test_release_staging_buffers_is_safe_without_gpu():
+    from paper_2501_02573_b200 import release_staging_buffers
+    release_staging_buffers()
+    release_staging_buffers()
