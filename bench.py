@@ -361,6 +361,10 @@ def run_ours(args):
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:   # torchrun sets OMP_NUM_THREADS=1: give each rank its share of host cores for
+        # the host-side copies of the e2e legs (pinned staging of numpy inputs)
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        torch.set_num_threads(max(1, len(os.sched_getaffinity(0)) // local_world))
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
