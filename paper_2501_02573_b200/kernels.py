@@ -27,6 +27,7 @@ There is no CPU fallback: without the CUDA library every method raises.
 from __future__ import annotations
 
 import enum
+import os
 import threading
 from dataclasses import dataclass
 
@@ -141,6 +142,27 @@ def _pieces(batch: int, heads: int, target: int = 16):
 _STAGING = threading.local()
 
 
+_COPY_POOL = None
+
+
+def _host_copy(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """dst.copy_(src) on the host, spread over the available cores when torch itself runs
+    single-threaded (torchrun sets OMP_NUM_THREADS=1); torch releases the GIL while copying."""
+    global _COPY_POOL
+    workers = min(len(os.sched_getaffinity(0)), 16)
+    if torch.get_num_threads() > 1 or workers <= 1 or dst.numel() < (1 << 21):
+        dst.copy_(src)
+        return
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _COPY_POOL = ThreadPoolExecutor(max_workers=workers, thread_name_prefix="linattn-copy")
+    d, s_ = dst.view(-1), src.reshape(-1)
+    step = -(-d.numel() // workers)
+    futures = [_COPY_POOL.submit(d[a:a + step].copy_, s_[a:a + step]) for a in range(0, d.numel(), step)]
+    for f in futures:
+        f.result()
+
+
 def release_staging_buffers() -> None:
     """Free the calling thread's cached pinned staging buffers (host-input ``run_method`` calls
     keep up to eight piece-sized page-locked buffers per thread for reuse)."""
@@ -205,7 +227,7 @@ def _host_pipelined(inputs: AttnInputs, cdt, run, result, pieces: int = 16):
                 src = host[bs, hs]
                 if staged_in:
                     stg = _staging(cdt, slot, role, src.numel()).view(src.shape)
-                    stg.copy_(src)                           # host copy + cast, all cores
+                    _host_copy(stg, src)                     # host copy + cast, all cores
                     d[bs, hs].copy_(stg, non_blocking=True)
                 elif src.dtype == cdt:
                     d[bs, hs].copy_(src, non_blocking=True)
@@ -229,13 +251,13 @@ def _host_pipelined(inputs: AttnInputs, cdt, run, result, pieces: int = 16):
             done.record(s_out)
         if pending is not None:                            # previous piece: widen into result
             pending[0].synchronize()
-            pending[2].copy_(pending[1])
+            _host_copy(pending[2], pending[1])
             pending = None
         if staged_out:
             pending = (done, ostg, result[bs, hs])
     if pending is not None:
         pending[0].synchronize()
-        pending[2].copy_(pending[1])
+        _host_copy(pending[2], pending[1])
     s_out.synchronize()
     return result.numpy() if numpy_in else result
 
