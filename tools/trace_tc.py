@@ -38,6 +38,9 @@ def main(mode="full", B=8, H=32, N=8192, d=128, cta=0):
             print(f"  {EV[e]:26s} rel. to dS issue of same chunk: median {np.median(rel):8.0f}")
     nb = B * H * ((d + 127) // 128)
     st, en, sm = t0[8, :nb], t0[9, :nb], t0[0, :nb]
+    live = st > 0                      # balanced launches run fewer CTAs (one per SM) than units
+    st, en, sm = st[live], en[live], sm[live]
+    nb = int(live.sum())
     t_min = st.min()
     print(f"CTAs {nb}: start span {(st.max() - t_min) / 1e3:.1f} us, end span {(en.min() - t_min) / 1e3:.1f}.."
           f"{(en.max() - t_min) / 1e3:.1f} us; CTA duration median {np.median(en - st) / 1e3:.1f} us "
