@@ -539,3 +539,24 @@ def test_numpy_inputs_concurrent_threads(la):
     for (_, _, i, m), out in got.items():
         assert isinstance(out, np.ndarray) and out.dtype == np.float32
         np.testing.assert_array_equal(out, serial[(i, m)])
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_decode_fuzz(la, seed):
+    """Random decode shapes (few or many states, ragged column slices, odd dv, bf16 / fp32 inputs):
+    several steps against the oracle recurrence, state and outputs."""
+    from paper_2501_02573_b200 import ops
+    rng = np.random.default_rng(500 + seed)
+    B, H = int(rng.choice([1, 2, 3, 40])), int(rng.choice([1, 3, 8]))
+    dk, dv = int(rng.choice([4, 16, 64, 128, 200])), int(rng.choice([4, 5, 36, 100, 128, 256]))
+    gam = [float(rng.choice([0.0, 0.5, 0.95, 1.0])) for _ in range(H)]
+    steps = 3
+    s0 = rng.standard_normal((B, H, dk, dv)) * 0.1
+    q, k, v = (rng.standard_normal((B, H, steps, d)) for d in (dk, dk, dv))
+    ref, ref_s = orc.decode_steps(q, k, v, s0, gam)
+    st = dev(s0)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    outs = [ops.decode_step(dev(q[:, :, i]), dev(k[:, :, i]), dev(v[:, :, i]), st, l2) for i in range(steps)]
+    got = torch.stack(outs, 2).cpu().numpy()
+    assert orc.max_rel_error(got, ref) <= TOL_F32, (B, H, dk, dv)
+    assert orc.max_rel_error(st.cpu().numpy(), ref_s) <= TOL_F32, (B, H, dk, dv)
