@@ -485,6 +485,13 @@ def test_random_shapes_fuzz(la, seed):
         out = ops.prefill(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_in=dev(s0), s_out=s_out, kernel=kernel)
         assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= tol, (dt, B, H, N, dk, dv)
         assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= max(tol, 5e-3), (dt, B, H, N, dk, dv)
+        # the row recurrence (b200-recurrent) on the same inputs, where its kernel takes the shape
+        ev = 16 // torch.tensor([], dtype=dt).element_size()
+        if dk % ev == 0 and dv % ev == 0 and dk <= 256:
+            s_rec = torch.empty_like(s_out)
+            rec = ops.recurrent(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_in=dev(s0), s_out=s_rec)
+            assert orc.max_rel_error(rec.float().cpu().numpy(), ref) <= tol, ("rec", dt, B, H, N, dk, dv)
+            assert orc.max_rel_error(s_rec.cpu().numpy(), ref_s) <= max(tol, 1e-5), ("rec", dt, B, H, N, dk, dv)
 
 
 def test_recurrent_lazy_renormalisation(la):
