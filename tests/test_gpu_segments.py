@@ -289,3 +289,34 @@ def test_state_pass_split(ops, dt):
     s1 = torch.empty_like(s)
     ops.prefill(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_out=s1, kernel=kernel, seq_split=1)
     assert orc.max_rel_error(s.cpu().numpy(), s1.cpu().numpy()) <= (2e-3 if dt == torch.bfloat16 else 1e-5)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_sp_fuzz(ops, seed):
+    """Sequence parallelism with the all-gather replaced by a stack: random rank counts, uneven
+    (possibly tiny) segments, head dims incl. dk=256, bf16 tensor cores and the fp32 FFMA backend."""
+    from paper_2501_02573_b200.sp import CudaBackend
+    rng = np.random.default_rng(700 + seed)
+    P = int(rng.choice([2, 3, 5, 8]))
+    dk, dv = [(64, 64), (128, 128), (128, 256), (256, 512)][int(rng.integers(0, 4))]
+    B, H = int(rng.choice([1, 2])), int(rng.choice([1, 3]))
+    cuts = np.sort(rng.choice(np.arange(1, 4000), size=P - 1, replace=False))
+    N = int(cuts[-1] + rng.integers(1, 800))
+    bounds = list(zip([0] + cuts.tolist(), cuts.tolist() + [N]))
+    gam = [float(rng.choice([0.0, 0.9, 1 - 2.0 ** -10, 1.0])) for _ in range(H)]
+    fp32 = bool(rng.integers(0, 2)) and dk <= 128
+    dt, tol, kernel = (torch.float32, TOL_F32, "simt") if fp32 else (torch.bfloat16, TOL_BF16, "auto")
+    b, c, v = orc.gen_inputs(B, H, N, dk, dv, np.float32, 800 + seed)
+    if not fp32:
+        b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    ref, _ = orc.seeded_blocked_attn(b, c, v, gam, True, None, block=64)
+    l2 = ops.log2_gamma(gam, True, "cuda")
+    be = CudaBackend(kernel)
+    lens = [hi - lo for lo, hi in bounds]
+    segs = [[dev(x[:, :, lo:hi], dt) for x in (b, c, v)] for lo, hi in bounds]
+    locals_ = [be.local_states(k, vv, l2) for _, k, vv in segs]
+    ends = torch.stack([end for _, end in locals_])
+    outs = [be.prefill(q, k, vv, l2, be.prefix_combine(ends, lens, r, l2) if r > 0 else None, data)
+            for r, ((q, k, vv), (data, _)) in enumerate(zip(segs, locals_))]
+    got = torch.cat(outs, dim=2).float().cpu().numpy()
+    assert orc.max_rel_error(got, ref) <= tol, (P, lens, dk, dv, fp32)
