@@ -11,11 +11,10 @@ batch ("scaling": "weak"); the timed region is bracketed by barrier +
 synchronize and the max over ranks is reported.
 
 Extra keys: ``roofline`` (dominant kernel vs MEASURED_PEAKS.json), ``cpu_baseline``
-(the oracle port of the reference's CPU blocking route on a bounded sample,
-rank 0 only), ``decode`` (configs[3] decode step), ``clocks`` (nvidia-smi during
+(the reference's CPU route from baseline/_ref over the whole batch, rank 0 only), ``decode`` (configs[3] decode step), ``clocks`` (nvidia-smi during
 the timed region), ``gpu_launches`` (our kernels launched in the timed region).
-``--impl reference`` times the reference's CPU algorithm (oracle port; the
-reference is pure Python/numpy and cannot travel to the GPU box) on rank 0.
+``--impl reference`` times the reference's own CPU route (linattn.run_method from
+baseline/_ref, the unmodified package; the oracle port only if it is absent) on rank 0.
 """
 
 from __future__ import annotations
@@ -55,31 +54,188 @@ def peaks():
 
 
 # --------------------------------------------------------------------------- CPU arm
+#
+# The reference's own CPU implementation of the path: ``linattn.run_method(TWO_LEVEL_BLOCK)``
+# (kernels.py:139-166; the LA analogue) from the unmodified package installed into
+# baseline/_ref (``__graft_entry__.build()``; pip --target), timed by the reference's protocol
+# (bench.py:87-125): inputs generated BEFORE the timer, warm-up runs, then repeats of
+# ``run_method(..., validate=False)`` under perf_counter, summarised by the reference's own
+# ``summarize`` (mean, n-1 std).  Two figures:
+#   * "pool": the configs[1] batch's (b, h) slices spread over one worker process per host core
+#     with one BLAS thread each (slices are independent) -- all the host threads;
+#   * "as_shipped": one process, BLAS at its default thread count, ``run_bench`` itself on a
+#     sample of the batch (the reference runs strictly sequentially).
+# Without baseline/_ref the numpy restatement in oracle/ stands in (kind "port").
 
-def _cpu_slice(args):
-    """One (b, h) slice of the reference CPU blocking route, f32 (oracle port)."""
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    from oracle import linattn_oracle as orc
-    n, dk, dv, gamma, seed = args
-    rng = np.random.default_rng(seed)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+REF_METHOD = "two-level-block"
+
+
+def _import_reference():
+    """The reference package from baseline/_ref, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "linattn")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import linattn
+    except Exception:  # a broken install: fall back to the port, and say so in the line
+        return None
+    return linattn
+
+
+def _slice_inputs(sid, n, dk, dv, gamma):
+    """Inputs of (b, h) slice `sid`: standard normal f32 like reference gen_inputs (bench.py:77-84),
+    seeded per slice so every worker builds only its own slices."""
+    rng = np.random.default_rng([0, sid, n, dk, dv])
     b = rng.standard_normal((1, 1, n, dk)).astype(np.float32)
     c = rng.standard_normal((1, 1, n, dk)).astype(np.float32)
     v = rng.standard_normal((1, 1, n, dv)).astype(np.float32)
-    t0 = time.perf_counter()
-    orc.blocked_attn(b, c, v, [gamma], True, block=C0)
-    return time.perf_counter() - t0
+    return b, c, v, gamma
 
 
-def cpu_sample(pool, cores, per_core=1, seed=0):
-    """Time cores*per_core slices of configs[1] in a process pool; tokens/s equivalent."""
-    g = gammas(CFG["H"])
-    jobs = [(CFG["N"], CFG["dk"], CFG["dv"], g[i % CFG["H"]], seed + i) for i in range(cores * per_core)]
-    t0 = time.perf_counter()
-    pool.map(_cpu_slice, jobs, chunksize=1)
-    dt = time.perf_counter() - t0
-    slices = len(jobs)
-    tokens = slices / (CFG["B"] * CFG["H"]) * CFG["B"] * CFG["N"]  # a token passes through all H heads
-    return tokens / dt, dt, slices
+def _ref_worker(conn, sids, n, dk, dv, gammas, use_ref):
+    """Pool worker: builds its slices' inputs (untimed), then times run_method per command."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    lib = _import_reference() if use_ref else None
+    if lib is not None:
+        method = lib.MethodId.parse(REF_METHOD)
+        params = lib.BlockParams()
+        inputs = []
+        for sid in sids:
+            b, c, v, g = _slice_inputs(sid, n, dk, dv, gammas[sid % len(gammas)])
+            inputs.append(lib.AttnInputs(b=b, c=c, v=v, gamma=[g], decay=True))
+            lib.validate_inputs(inputs[-1])
+        run = lambda inp: lib.run_method(method, inp, params, validate=False)   # noqa: E731
+    else:
+        from oracle import linattn_oracle as orc
+        inputs = [_slice_inputs(sid, n, dk, dv, gammas[sid % len(gammas)]) for sid in sids]
+        run = lambda inp: orc.blocked_attn(inp[0], inp[1], inp[2], [inp[3]], True, block=C0)   # noqa: E731
+    conn.send("ready")
+    while True:
+        cmd = conn.recv()
+        if cmd is None:
+            break
+        times = []
+        for inp in inputs:
+            t0 = time.perf_counter()
+            run(inp)
+            times.append(time.perf_counter() - t0)
+        conn.send(times)
+    conn.close()
+
+
+class RefPool:
+    """One worker process per core, each owning a fixed share of the (b, h) slices."""
+
+    def __init__(self, slices, workers, n, dk, dv, gammas, use_ref):
+        ctx = mproc.get_context("spawn")
+        self.conns, self.procs = [], []
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"          # inherited by the spawned workers
+        for w in range(workers):
+            mine = list(range(w, slices, workers))
+            if not mine:
+                continue
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_ref_worker, args=(b, mine, n, dk, dv, gammas, use_ref), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        for c in self.conns:
+            assert c.recv() == "ready"
+        self.slices = slices
+
+    def step(self):
+        """Wall time of one pass over every slice (all workers concurrently) + per-slice times."""
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send("run")
+        per = [t for c in self.conns for t in c.recv()]
+        return time.perf_counter() - t0, per
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for p in self.procs:
+            p.join(timeout=30)
+
+
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), model)
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": i.get("internal_api"), "version": i.get("version"), "threads": i.get("num_threads")}
+                for i in threadpool_info() if i.get("user_api") == "blas"]
+    except Exception:
+        pass
+    return {"cpu_model": model, "cores": cores_available(), "blas": blas, "numpy": np.__version__}
+
+
+def as_shipped(lib, heads=8, repeats=3):
+    """The reference's run_bench (one process, default BLAS threads) on a 1 x heads x 8192 x 128
+    sample of configs[1], both blocking routes; per-slice seconds (mean, std)."""
+    cfg = lib.BenchConfig(methods=[lib.MethodId.TWO_LEVEL_BLOCK, lib.MethodId.BLOCK_BASED],
+                          grid=[(1, heads, CFG["N"], CFG["dk"], CFG["dv"])], decay=True,
+                          gamma=gammas(CFG["H"])[CFG["H"] // 2], dtype=np.float32, repeats=repeats, warmup=1)
+    rep = lib.run_bench(cfg)
+    return {r.method.value: {"per_slice_ms": 1e3 * r.mean_s / heads, "std_ms": 1e3 * r.std_s / heads,
+                             "tokens_per_s": CFG["B"] * CFG["N"] / (r.mean_s / heads * CFG["B"] * CFG["H"])}
+            for r in rep.rows if r.status == "ok"}
+
+
+def cpu_arm(steps, warmup, seconds=None):
+    """Time the reference CPU route on configs[1]: `steps` timed passes over the whole batch
+    (or, with `seconds`, as many passes as fit, at least one).  Returns a dict for the line."""
+    lib = _import_reference()
+    kind = "reference" if lib is not None else "port"
+    cores = cores_available()
+    slices = CFG["B"] * CFG["H"]
+    pool = RefPool(slices, cores, CFG["N"], CFG["dk"], CFG["dv"], gammas(CFG["H"]), lib is not None)
+    try:
+        for _ in range(warmup):
+            pool.step()
+        walls, per = [], []
+        while True:
+            wall, p = pool.step()
+            walls.append(wall)
+            per.extend(p)
+            if seconds is None and len(walls) >= steps:
+                break
+            if seconds is not None and sum(walls) >= seconds:
+                break
+    finally:
+        pool.close()
+    if lib is not None:
+        mean, std = lib.summarize(walls)
+    else:
+        mean, std = float(np.mean(walls)), float(np.std(walls, ddof=1)) if len(walls) > 1 else 0.0
+    tokens = CFG["B"] * CFG["N"]              # one pass = the whole configs[1] batch
+    out = {"value": tokens / mean, "unit": "tokens/s", "cores": cores, "kind": kind,
+           "ms_per_step": 1e3 * mean, "std_ms": 1e3 * std, "passes": len(walls),
+           "per_slice_ms": 1e3 * float(np.mean(per)),
+           "sample": (f"the whole configs[1] batch (B=8,H=32,N=8192,d=128 f32, {slices} (b,h) slices) per pass, "
+                      f"{len(walls)} timed passes after {warmup} warm-up; "
+                      + (f"linattn.run_method({REF_METHOD}, validate=False) from baseline/_ref"
+                         if lib is not None else "oracle port of two-level-block (baseline/_ref absent)")
+                      + f", inputs generated before the timer, {len(pool.conns)} worker processes x 1 BLAS thread"),
+           "host": host_info()}
+    if lib is not None:
+        try:
+            out["as_shipped"] = as_shipped(lib)
+        except Exception as exc:  # informational only
+            out["as_shipped"] = {"error": repr(exc)}
+    return out
 
 
 def cores_available():
@@ -93,28 +249,17 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cores = cores_available()
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    ctx = mproc.get_context("spawn")
-    with ctx.Pool(cores) as pool:
-        for _ in range(args.warmup):
-            cpu_sample(pool, cores)
-        vals, times = [], []
-        for i in range(args.steps):
-            v, dt, slices = cpu_sample(pool, cores, seed=1000 + i)
-            vals.append(v)
-            times.append(dt)
-    value = float(np.mean(vals))
-    sample = (f"{slices} of {CFG['B'] * CFG['H']} (b,h) slices of configs[1] per step, f32, "
-              f"two-level-block chunk {C0}, process pool x{cores}")
+    arm = cpu_arm(args.steps, args.warmup)
+    value = arm["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "configs[1] chunked prefill B=8,H=32,N=8192,d=128 (bounded CPU sample)",
-                   "global_batch": CFG["B"], "seq_len": CFG["N"], "parallelism": "cpu-process-pool"},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+        "n_gpus": args.gpus, "steps": arm["passes"], "warmup": args.warmup,
+        "ms_per_step": arm["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (standard normal, seeded per slice)",
+        "config": {"workload": "configs[1] chunked prefill B=8,H=32,N=8192,d=128 (the reference CPU route, f32)",
+                   "global_batch": CFG["B"], "seq_len": CFG["N"], "heads": CFG["H"],
+                   "parallelism": f"cpu process pool x{arm['cores']}", "method": REF_METHOD},
+        "cpu_baseline": arm,
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -469,24 +614,10 @@ def run_ours(args):
     cfg5 = None if args.no_extra else bench_seqpar(args, ops, dev, g, hbm, world, rank, barrier, max_over_ranks)
     f32 = None if args.no_extra else bench_fp32(args, ops, dev, g, hbm, barrier, max_over_ranks)
 
-    # CPU baseline (oracle port of the reference's CPU blocking route), rank 0 at N=1 only
+    # CPU baseline: the reference's own CPU route (baseline/_ref), rank 0 at N=1 only, ~10 s
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cores = cores_available()
-        os.environ["OPENBLAS_NUM_THREADS"] = "1"
-        with mproc.get_context("spawn").Pool(cores) as pool:
-            cpu_sample(pool, cores)                       # warm the workers
-            total_t, total_slices, rounds = 0.0, 0, 0
-            while total_t < args.cpu_seconds:             # ~10 s of CPU work by default
-                _, cdt, slices = cpu_sample(pool, cores, per_core=4, seed=77 + rounds)
-                total_t += cdt
-                total_slices += slices
-                rounds += 1
-        cv = total_slices / (B * H) * B * N / total_t
-        cpu = {"value": cv, "unit": "tokens/s", "cores": cores, "kind": "port",
-               "sample": f"{total_slices} (b,h) slices of configs[1] ({total_slices / (B * H):.1f} x the batch), "
-                         f"f32 two-level-block chunk {C0} (oracle/linattn_oracle.py), process pool x{cores}, "
-                         f"{total_t:.1f} s"}
+        cpu = cpu_arm(0, 1, seconds=args.cpu_seconds)
 
     kernel_name = ops.prefill_kernel_name(dk, dv, torch.bfloat16, kernel)
     line = {
@@ -541,7 +672,30 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     return run_ours(args)
+
+
+def relaunch(n):
+    """--gpus N outside torchrun: re-run this command as N ranks (one process per GPU)."""
+    import socket
+    import subprocess
+    if os.environ.get("LINATTN_BENCH_BACKEND", "nccl") == "nccl":
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            raise SystemExit(f"bench.py: --gpus {n} needs {n} GPUs for NCCL, this host has {have} "
+                             "(LINATTN_BENCH_BACKEND=gloo runs the ranks on shared GPUs as a path check)")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define LINATTN_ABI_VERSION 2
+#define LINATTN_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define LINATTN_API __attribute__((visibility("default")))
@@ -157,6 +157,16 @@ LINATTN_API int linattn_recurrent(const void* q, const void* k, const void* v, v
 
 /* Kernel family LINATTN_KERNEL_AUTO resolves to for this shape/dtype (TC or SIMT). */
 LINATTN_API int linattn_prefill_kernel(int64_t dk, int64_t dv, int dtype);
+
+/* Finiteness scan of the entry contract (reference check_finite, tensor.py:20-25), one HBM pass:
+ * atomically lowers *first_bad (DEVICE int64, initialised by the caller to INT64_MAX) to the
+ * smallest flat index of a NaN/Inf among the n elements of x (dtype f32 or bf16).  Scanning q, k
+ * and v into three slots needs a single synchronisation to read the verdicts back. */
+LINATTN_API int linattn_nonfinite_index(const void* x, int64_t n, int dtype, int64_t* first_bad, void* stream);
+
+/* Return the library's cached split/balance workspace memory (stream-ordered pools, one per
+ * device) to the driver; up to 256 MiB per device is otherwise kept mapped between calls. */
+LINATTN_API int linattn_release_workspace(void);
 
 /* Thread-local message for the last non-OK status returned on this thread. */
 LINATTN_API const char* linattn_last_error(void);

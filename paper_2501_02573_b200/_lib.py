@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("LINATTN_LIB") or os.path.join(
 OK, ESHAPE, EPARAM, EDTYPE, EUNSUPPORTED, ECUDA = range(6)
 F32, BF16 = 0, 1
 KERNEL_AUTO, KERNEL_TC, KERNEL_SIMT = 0, 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lib = None
 
@@ -40,6 +40,8 @@ _SIGS = {
                                   _i64, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _i64, _vp],
     "linattn_segment_prefix": [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
     "linattn_state_at": [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
+    "linattn_nonfinite_index": [_vp, _i64, ctypes.c_int, _vp, _vp],
+    "linattn_release_workspace": [],
     "linattn_last_error": [],
     "linattn_abi_version": [],
     "linattn_launch_count": [],

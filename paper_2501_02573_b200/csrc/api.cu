@@ -72,25 +72,36 @@ static int sm_count() {
   return v;
 }
 
-// Library-owned stream-ordered pool for split workspaces (never trimmed: no re-mapping per call).
+// Library-owned stream-ordered pool for split workspaces.  Up to kPoolKeep bytes stay mapped
+// between calls (no re-mapping per call at the benchmark shapes); anything above is returned to
+// the driver at the next stream synchronisation, and linattn_release_workspace() trims it all.
+static constexpr uint64_t kPoolKeep = 256ull << 20;
+static cudaMemPool_t g_pools[64] = {};
+static std::mutex g_pool_mu;
+
 static cudaMemPool_t work_pool() {
-  static cudaMemPool_t pools[64] = {};
-  static std::mutex mu;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (!pools[dev]) {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  if (!g_pools[dev]) {
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;
     props.location.id = dev;
     cudaMemPool_t p = nullptr;
     if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
-    uint64_t keep = ~0ull;
+    uint64_t keep = kPoolKeep;
     cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
-    pools[dev] = p;
+    g_pools[dev] = p;
   }
-  return pools[dev];
+  return g_pools[dev];
+}
+
+static int trim_pools() {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  for (auto& p : g_pools)
+    if (p && cudaMemPoolTrimTo(p, 0) != cudaSuccess) return LINATTN_ECUDA;
+  return LINATTN_OK;
 }
 
 // Sub-segment length of a segment of seg_len tokens split m ways (multiple of the TC chunk).
@@ -435,6 +446,19 @@ int linattn_recurrent(const void* q, const void* k, const void* v, void* o, cons
                 "(got %lld, %lld)", (long long)dk, (long long)dv);
   return cuda_status(launch_recurrent(q, k, v, o, log2g, s_in, s_out, s, dtype, (cudaStream_t)stream),
                      "recurrent");
+}
+
+int linattn_nonfinite_index(const void* x, int64_t n, int dtype, int64_t* first_bad, void* stream) {
+  if (int e = check_dtype(dtype)) return e;
+  if (n < 0) return fail(LINATTN_ESHAPE, "element count must be >= 0, got %lld", (long long)n);
+  if ((!x && n > 0) || !first_bad) return fail(LINATTN_EPARAM, "null pointer");
+  if (n == 0) return LINATTN_OK;
+  return cuda_status(launch_nonfinite(x, n, dtype, first_bad, (cudaStream_t)stream), "nonfinite_index");
+}
+
+int linattn_release_workspace(void) {
+  if (trim_pools() != LINATTN_OK) return fail(LINATTN_ECUDA, "cudaMemPoolTrimTo failed");
+  return LINATTN_OK;
 }
 
 int linattn_prefill_kernel(int64_t dk, int64_t dv, int dtype) {

@@ -220,6 +220,10 @@ cudaError_t launch_prefix_combine(const float* gathered, float* s_in, const int6
                                   int P, int rank, const float* log2g, const ShapeArgs& s,
                                   cudaStream_t stream);
 
+// Lowers *first_bad (device int64, caller-initialised to INT64_MAX) to the smallest flat index of a
+// NaN/Inf element among the n elements of x (f32 or bf16): one coalesced read.
+cudaError_t launch_nonfinite(const void* x, int64_t n, int dtype, int64_t* first_bad, cudaStream_t stream);
+
 void count_launch();
 
 }  // namespace linattn

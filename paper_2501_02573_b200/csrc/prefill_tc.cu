@@ -712,16 +712,6 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
   const size_t per_state = (size_t)gridDim.y * DK * dv;
   int* wl = reinterpret_cast<int*>(tmem_slot + 2);   // BAL: ticket of this cluster's range
 
-  if constexpr (!BAL) {
-    const float lg0 = log2g[blockIdx.y % H];
-    if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg0, (float)threadIdx.x);
-    if (threadIdx.x < 192) {
-      const int k = (int)threadIdx.x - 64;
-      const float a = k >= 0 ? gpow(lg0, (float)k) : 0.f;
-      const float b = k + 1 >= 0 ? gpow(lg0, (float)(k + 1)) : 0.f;
-      pw2[k] = pack_bf16x2(a, b);
-    }
-  }
   if (warp == 2 && lane == 0) {
     if constexpr (BAL) {
       // one ticket per cluster (start order); rank 0 takes it and parks it in global memory for
@@ -765,7 +755,19 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     if (threadIdx.x == 0) *wl = (int)__ldcg(bal.flags + gridDim.x + 1 + blockIdx.x / MC);
     __syncthreads();
   }
-  if constexpr (!BAL) pdl_wait();   // everything above overlapped the previous kernel's tail
+  if constexpr (!BAL) {
+    pdl_wait();   // everything above overlapped the previous kernel's tail
+    // the gamma tables read log2g, which an earlier kernel in the stream may have written
+    const float lg0 = log2g[blockIdx.y % H];
+    if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg0, (float)threadIdx.x);
+    if (threadIdx.x < 192) {
+      const int k = (int)threadIdx.x - 64;
+      const float a = k >= 0 ? gpow(lg0, (float)k) : 0.f;
+      const float b = k + 1 >= 0 ? gpow(lg0, (float)(k + 1)) : 0.f;
+      pw2[k] = pack_bf16x2(a, b);
+    }
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   const uint32_t crank = MC > 1 ? cluster_ctarank() : 0;

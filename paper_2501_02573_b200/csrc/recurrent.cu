@@ -82,7 +82,7 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
   };
   const int nchunks = (N + TC - 1) / TC;
   float sig = 1.f, inv = 1.f;                                // lazy decay state (see token_loop)
-  const float ginv = g > 0.f ? 1.f / g : 0.f;
+  const float ginv = g >= 0x1p-30f ? 1.f / g : 0.f;
   if (nchunks > 0) stage(0, 0);
   for (int ci = 0; ci < nchunks; ++ci) {
     const int c0 = ci * TC, buf = ci & 1;
@@ -158,8 +158,9 @@ recurrent_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
      }
     };
     // (fp32 inputs keep the direct form: the lazy variant spills there and measured slower)
+    // gamma < 2^-30 keeps the direct form too: 1/gamma (and k / sig) would overflow to inf
     if constexpr (sizeof(T) == 2) {
-      if (g > 0.f) token_loop(std::true_type{});
+      if (g >= 0x1p-30f) token_loop(std::true_type{});
       else token_loop(std::false_type{});
     } else {
       token_loop(std::false_type{});

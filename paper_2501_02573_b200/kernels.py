@@ -165,8 +165,14 @@ def _host_copy(dst: torch.Tensor, src: torch.Tensor) -> None:
 
 def release_staging_buffers() -> None:
     """Free the calling thread's cached pinned staging buffers (host-input ``run_method`` calls
-    keep up to eight piece-sized page-locked buffers per thread for reuse)."""
+    keep up to eight piece-sized page-locked buffers per thread for reuse) and return the
+    library's cached device workspace (sequence-split / balanced-schedule pools) to the driver."""
     _STAGING.__dict__.pop("bufs", None)
+    if torch.cuda.is_available():
+        from . import _lib
+        lib = _lib.load()
+        torch.cuda.synchronize()           # pool frees are stream-ordered
+        _lib.check(lib.linattn_release_workspace())
 
 
 def _staging(dtype, slot: int, role: int, numel: int) -> torch.Tensor:

@@ -10,6 +10,7 @@ Every call is asynchronous on torch's current CUDA stream.
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import numpy as np
 import torch
@@ -22,8 +23,10 @@ _KERNELS = {"auto": _lib.KERNEL_AUTO, "tc": _lib.KERNEL_TC, "simt": _lib.KERNEL_
 
 
 def _require_cuda(*ts):
+    """Every given tensor is a contiguous CUDA tensor, all on one device."""
     if not torch.cuda.is_available():
         raise LinAttnError("no CUDA device: the B200 path has no CPU fallback")
+    dev = None
     for t in ts:
         if t is None:
             continue
@@ -31,6 +34,55 @@ def _require_cuda(*ts):
             raise UsageError("tensor is not on a CUDA device")
         if not t.is_contiguous():
             raise UsageError("tensor must be contiguous")
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise UsageError(f"tensors on different devices: {dev} and {t.device}")
+
+
+def _on_tensor_device(fn):
+    """Run ``fn`` with its first tensor argument's CUDA device current.
+
+    The library reads cudaGetDevice() (SM count, workspace pool, kernel attributes) and every
+    launch goes to torch's current stream of the current device, so a call with tensors on
+    cuda:1 while cuda:0 is current must switch devices first.
+    """
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        t0 = next((a for a in args if isinstance(a, torch.Tensor)), None)
+        if t0 is None or not t0.is_cuda or t0.device == torch.device("cuda", torch.cuda.current_device()):
+            return fn(*args, **kwargs)
+        with torch.cuda.device(t0.device):
+            return fn(*args, **kwargs)
+    return wrapper
+
+
+def _check_kv(k, v, ndim: int = 4):
+    """k [..., dk] and v [..., dv] agree on every leading axis and share a dtype."""
+    if k.dim() != ndim or v.dim() != ndim or tuple(v.shape[:-1]) != tuple(k.shape[:-1]):
+        raise ShapeError(f"expected k [..., dk] and v [..., dv] with {ndim} dims and equal leading axes; "
+                         f"got {tuple(k.shape)}, {tuple(v.shape)}")
+    if k.dtype != v.dtype:
+        raise UsageError(f"dtype mismatch: k={k.dtype} v={v.dtype}")
+
+
+def _check_qkv(q, k, v, ndim: int = 4):
+    """q, k [..., dk] of equal shape and v [..., dv] agreeing on the leading axes; one dtype."""
+    _check_kv(k, v, ndim)
+    if tuple(q.shape) != tuple(k.shape):
+        raise ShapeError(f"q and k must have the same shape; got {tuple(q.shape)}, {tuple(k.shape)}")
+    if q.dtype != k.dtype:
+        raise UsageError(f"dtype mismatch: q={q.dtype} k={k.dtype} v={v.dtype}")
+
+
+def _check_state(st, shape, what="state"):
+    if st is not None and (st.dtype != torch.float32 or tuple(st.shape) != tuple(shape)):
+        raise ShapeError(f"{what} must be float32 {list(shape)}, got {st.dtype} {tuple(st.shape)}")
+
+
+def _check_log2g(log2g, heads: int):
+    if log2g.dtype != torch.float32 or log2g.dim() != 1 or log2g.shape[0] < heads:
+        raise ShapeError(f"log2g must be float32 [H] with H >= {heads}, got {log2g.dtype} {tuple(log2g.shape)}")
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -80,6 +132,7 @@ def _batch_chunks(B: int, H: int):
     return [(b0, min(B, b0 + step)) for b0 in range(0, B, step)]
 
 
+@_on_tensor_device
 def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "auto",
             seq_split: int | None = None):
     """O = (Q K^T (.) M_gamma) V on device; optional initial/end state (fp32).
@@ -102,18 +155,16 @@ def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "a
     if seq_split == 1:
         return prefill_segmented(q, k, v, log2g, q.shape[2], s_in=s_in, s_out=s_out, out=out, kernel=kernel)
     _require_cuda(q, k, v, log2g, s_in, s_out, out)
-    if not (q.dtype == k.dtype == v.dtype):
-        raise UsageError(f"dtype mismatch: q={q.dtype} k={k.dtype} v={v.dtype}")
-    if q.dim() != 4 or k.shape != q.shape or v.dim() != 4 or v.shape[:3] != q.shape[:3]:
-        raise ShapeError(f"expected q,k [B,H,N,dk] and v [B,H,N,dv]; got {tuple(q.shape)}, "
-                         f"{tuple(k.shape)}, {tuple(v.shape)}")
+    _check_qkv(q, k, v)
     B, H, N, dk = q.shape
     dv = v.shape[3]
+    _check_log2g(log2g, H)
     if out is None:
         out = torch.empty_like(v)
+    if tuple(out.shape) != tuple(v.shape) or out.dtype != v.dtype:
+        raise ShapeError(f"out must be {v.dtype} {tuple(v.shape)}, got {out.dtype} {tuple(out.shape)}")
     for st in (s_in, s_out):
-        if st is not None and (st.dtype != torch.float32 or tuple(st.shape) != (B, H, dk, dv)):
-            raise ShapeError(f"state must be float32 [B,H,dk,dv]={B, H, dk, dv}, got {tuple(st.shape)}")
+        _check_state(st, (B, H, dk, dv))
     lib = _lib.load()
     for b0, b1 in _batch_chunks(B, H):   # more than 65535 (batch, head) units: one launch per chunk
         sl = (lambda t: None if t is None else t[b0:b1])   # noqa: E731
@@ -123,11 +174,15 @@ def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "a
     return out
 
 
+@_on_tensor_device
 def state_pass(k, v, log2g, *, s_out=None, kernel: str = "auto"):
     """End state sum_t gamma^(N-1-t) k_t^T v_t of each (b, h) segment (fp32)."""
     _require_cuda(k, v, log2g, s_out)
+    _check_kv(k, v)
     B, H, N, dk = k.shape
     dv = v.shape[3]
+    _check_log2g(log2g, H)
+    _check_state(s_out, (B, H, dk, dv), "s_out")
     if s_out is None:
         s_out = torch.empty((B, H, dk, dv), dtype=torch.float32, device=k.device)
     lib = _lib.load()
@@ -146,6 +201,7 @@ def seq_plan(B: int, H: int, N: int, dk: int, dv: int, dtype=torch.bfloat16, ker
     return tuple(int(x) for x in plan)
 
 
+@_on_tensor_device
 def state_pass_segmented(k, v, log2g, seg_len: int, *, m: int = 1, nseg: int | None = None,
                          kernel: str = "auto", out=None):
     """Local end states of segments [p*seg_len, (p+1)*seg_len), each cut into m sub-segments.
@@ -153,10 +209,13 @@ def state_pass_segmented(k, v, log2g, seg_len: int, *, m: int = 1, nseg: int | N
     Returns [nseg*m, B, H, dk, dv] fp32 (each sub-segment from a zero state).
     """
     _require_cuda(k, v, log2g, out)
+    _check_kv(k, v)
     B, H, N, dk = k.shape
     dv = v.shape[3]
+    _check_log2g(log2g, H)
     if nseg is None:
         nseg = -(-N // seg_len)
+    _check_state(out, (nseg * m, B, H, dk, dv), "out")
     if out is None:
         out = torch.empty((nseg * m, B, H, dk, dv), dtype=torch.float32, device=k.device)
     lib = _lib.load()
@@ -166,6 +225,7 @@ def state_pass_segmented(k, v, log2g, seg_len: int, *, m: int = 1, nseg: int | N
     return out
 
 
+@_on_tensor_device
 def segment_prefix(loc, loc_geom, seg_len: int, nseg: int, log2g, n: int, *, out=None):
     """Inclusive prefix states incl[p] at token min(n, (p+1)*seg_len), p < nseg, from the local
     states ``loc`` of ``state_pass_segmented`` (geometry ``loc_geom``); [nseg, B, H, dk, dv]."""
@@ -179,19 +239,25 @@ def segment_prefix(loc, loc_geom, seg_len: int, nseg: int, log2g, n: int, *, out
     return out
 
 
+@_on_tensor_device
 def prefill_segmented(q, k, v, log2g, seg_len: int, *, loc=None, loc_geom=None, inclusive: bool = False,
                       s_in=None, s_out=None, out=None, kernel: str = "auto"):
     """Prefill with every seg_len-token segment in parallel, seeded from s_in and ``loc``: local
     states from ``state_pass_segmented`` (geometry ``loc_geom = (seg_len, m)``), or, with
     ``inclusive``, prefix states from ``segment_prefix`` (one read per segment)."""
     _require_cuda(q, k, v, log2g, s_in, s_out, out, loc)
+    _check_qkv(q, k, v)
     B, H, N, dk = q.shape
     dv = v.shape[3]
+    _check_log2g(log2g, H)
     if out is None:
         out = torch.empty_like(v)
+    if tuple(out.shape) != tuple(v.shape) or out.dtype != v.dtype:
+        raise ShapeError(f"out must be {v.dtype} {tuple(v.shape)}, got {out.dtype} {tuple(out.shape)}")
     for st in (s_in, s_out):
-        if st is not None and (st.dtype != torch.float32 or tuple(st.shape) != (B, H, dk, dv)):
-            raise ShapeError(f"state must be float32 [B,H,dk,dv]={B, H, dk, dv}, got {tuple(st.shape)}")
+        _check_state(st, (B, H, dk, dv))
+    if loc is not None and (loc.dim() != 5 or tuple(loc.shape[1:]) != (B, H, dk, dv) or loc.dtype != torch.float32):
+        raise ShapeError(f"loc must be float32 [n, B, H, dk, dv], got {loc.dtype} {tuple(loc.shape)}")
     lseg, lm = loc_geom if loc_geom is not None else (seg_len, 1)
     nloc = 0 if loc is None else loc.shape[0]
     lib = _lib.load()
@@ -202,6 +268,7 @@ def prefill_segmented(q, k, v, log2g, seg_len: int, *, loc=None, loc_geom=None, 
     return out
 
 
+@_on_tensor_device
 def state_at(loc, loc_geom, pos: int, log2g, n: int, *, s_in=None, out=None):
     """gamma^pos s_in + sum over loc entries ending at or before pos of gamma^(pos - hi) loc[z]."""
     _require_cuda(loc, log2g, s_in, out)
@@ -214,6 +281,7 @@ def state_at(loc, loc_geom, pos: int, log2g, n: int, *, s_in=None, out=None):
     return out
 
 
+@_on_tensor_device
 def prefix_combine(gathered, seg_lens, rank: int, log2g, *, s_in=None):
     """Exclusive gamma-weighted prefix of gathered [P,B,H,dk,dv] end states."""
     _require_cuda(gathered, log2g, s_in)
@@ -227,17 +295,22 @@ def prefix_combine(gathered, seg_lens, rank: int, log2g, *, s_in=None):
     return s_in
 
 
+@_on_tensor_device
 def decode_step(q, k, v, state, log2g, *, out=None):
     """S <- gamma S + k^T v ; o = q S for single tokens q,k [B,H,dk], v [B,H,dv]."""
     _require_cuda(q, k, v, state, log2g, out)
     if state.dtype != torch.float32:
         raise UsageError("decode state must be float32")
-    B, H, dk = q.shape[0], q.shape[1], q.shape[-1]
+    _check_qkv(q, k, v, ndim=3)
+    B, H, dk = q.shape
     dv = v.shape[-1]
+    _check_log2g(log2g, H)
     if tuple(state.shape) != (B, H, dk, dv):
         raise ShapeError(f"state must be [B,H,dk,dv]={B, H, dk, dv}, got {tuple(state.shape)}")
     if out is None:
         out = torch.empty_like(v)
+    if tuple(out.shape) != tuple(v.shape) or out.dtype != v.dtype:
+        raise ShapeError(f"out must be {v.dtype} {tuple(v.shape)}, got {out.dtype} {tuple(out.shape)}")
     lib = _lib.load()
     _lib.check(lib.linattn_decode_step(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                        state.data_ptr(), log2g.data_ptr(), B, H, dk, dv,
@@ -245,13 +318,20 @@ def decode_step(q, k, v, state, log2g, *, out=None):
     return out
 
 
+@_on_tensor_device
 def recurrent(q, k, v, log2g, *, s_in=None, s_out=None, out=None):
     """Row recurrence over whole sequences in one launch (S <- gamma S + k^T v; o = q S)."""
     _require_cuda(q, k, v, log2g, s_in, s_out, out)
+    _check_qkv(q, k, v)
     B, H, N, dk = q.shape
     dv = v.shape[3]
+    _check_log2g(log2g, H)
+    for st in (s_in, s_out):
+        _check_state(st, (B, H, dk, dv))
     if out is None:
         out = torch.empty_like(v)
+    if tuple(out.shape) != tuple(v.shape) or out.dtype != v.dtype:
+        raise ShapeError(f"out must be {v.dtype} {tuple(v.shape)}, got {out.dtype} {tuple(out.shape)}")
     lib = _lib.load()
     for b0, b1 in _batch_chunks(B, H):
         sl = (lambda t: None if t is None else t[b0:b1])   # noqa: E731
