@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("LINATTN_LIB") or os.path.join(
 
 OK, ESHAPE, EPARAM, EDTYPE, EUNSUPPORTED, ECUDA = range(6)
 F32, BF16 = 0, 1
-KERNEL_AUTO, KERNEL_TC, KERNEL_SIMT = 0, 1, 2
+KERNEL_AUTO, KERNEL_TC, KERNEL_SIMT, KERNEL_TF32 = 0, 1, 2, 3
 ABI_VERSION = 3
 
 _lib = None

@@ -14,6 +14,7 @@
 
 namespace linattn {
 
+extern float* g_tf32_dump;
 static thread_local std::string g_last_error;
 static thread_local int64_t g_launches = 0;
 
@@ -165,6 +166,43 @@ static int check_dtype(int dtype) {
   return LINATTN_OK;
 }
 
+// Kernel families: tcgen05 bf16 (TC), tcgen05 3xTF32 fp32 parity mode (TF32), FFMA (SIMT).
+enum Fam { FAM_TC, FAM_TF32, FAM_SIMT };
+
+static const char* fam_name(Fam f) {
+  return f == FAM_TC ? "prefill_tc" : f == FAM_TF32 ? "prefill_tf32" : "prefill_simt";
+}
+
+// AUTO: bf16 -> TC, fp32 -> TF32 (when the shape and alignment allow), else the FFMA kernel.
+static int pick_family(const ShapeArgs& s, int dtype, int kernel, std::initializer_list<const void*> ptrs, Fam& fam) {
+  if (kernel < LINATTN_KERNEL_AUTO || kernel > LINATTN_KERNEL_TF32)
+    return fail(LINATTN_EPARAM, "unknown kernel selector %d", kernel);
+  const bool al = aligned16(ptrs);
+  const bool tc_ok = tc_supported(s, dtype) && al;
+  const bool tf_ok = tf32_supported(s, dtype) && al;
+  if (kernel == LINATTN_KERNEL_TC && !tc_ok)
+    return fail(LINATTN_EUNSUPPORTED,
+                "tensor-core prefill needs bf16, dk in {64,128,256}, dv %% 64 == 0 and 16-byte aligned "
+                "tensors (got dtype=%d dk=%lld dv=%lld)", dtype, (long long)s.dk, (long long)s.dv);
+  if (kernel == LINATTN_KERNEL_TF32 && !tf_ok)
+    return fail(LINATTN_EUNSUPPORTED,
+                "3xTF32 prefill needs f32, dk <= 128, dk and dv multiples of 4 and 16-byte aligned tensors "
+                "(got dtype=%d dk=%lld dv=%lld)", dtype, (long long)s.dk, (long long)s.dv);
+  if (kernel == LINATTN_KERNEL_TC) fam = FAM_TC;
+  else if (kernel == LINATTN_KERNEL_TF32) fam = FAM_TF32;
+  else if (kernel == LINATTN_KERNEL_SIMT) fam = FAM_SIMT;
+  else fam = tc_ok ? FAM_TC : tf_ok ? FAM_TF32 : FAM_SIMT;
+  return LINATTN_OK;
+}
+
+static cudaError_t launch_fam(Fam f, const void* q, const void* k, const void* v, void* o, const float* log2g,
+                              const float* si, float* so, const ShapeArgs& s, int dtype, bool state_only,
+                              const SegArgs& a, int nz, cudaStream_t st) {
+  if (f == FAM_TC) return launch_prefill_tc(q, k, v, o, log2g, si, so, s, state_only, a, nz, st);
+  if (f == FAM_TF32) return launch_prefill_tf32(q, k, v, o, log2g, si, so, s, state_only, a, nz, st);
+  return launch_prefill_simt(q, k, v, o, log2g, si, so, s, dtype, state_only, a, nz, st);
+}
+
 }  // namespace linattn
 
 using namespace linattn;
@@ -180,21 +218,15 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
   if (!q || !k || !v || !o || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
   cudaStream_t st = (cudaStream_t)stream;
   // TMA needs 16-byte aligned bases; AUTO routes an unaligned view to the FFMA kernel
-  const bool tc_ok = tc_supported(s, dtype) && aligned16({q, k, v, o});
-  if (kernel == LINATTN_KERNEL_TC && !tc_ok)
-    return fail(LINATTN_EUNSUPPORTED,
-                "tensor-core prefill needs bf16, dk in {64,128,256}, dv %% 64 == 0 and 16-byte aligned "
-                "tensors (got dtype=%d dk=%lld dv=%lld)", dtype, (long long)dk, (long long)dv);
-  if (kernel != LINATTN_KERNEL_AUTO && kernel != LINATTN_KERNEL_TC && kernel != LINATTN_KERNEL_SIMT)
-    return fail(LINATTN_EPARAM, "unknown kernel selector %d", kernel);
-  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_ok;
+  Fam fam;
+  if (int e = pick_family(s, dtype, kernel, {q, k, v, o}, fam)) return e;
+  const bool tc = fam == FAM_TC;
   auto launch = [&](const void* q_, const void* o_, const float* si, float* so, bool state_only,
                     const SegArgs& a, int nz) {
-    return tc ? launch_prefill_tc(q_, k, v, (void*)o_, log2g, si, so, s, state_only, a, nz, st)
-              : launch_prefill_simt(q_, k, v, (void*)o_, log2g, si, so, s, dtype, state_only, a, nz, st);
+    return launch_fam(fam, q_, k, v, (void*)o_, log2g, si, so, s, dtype, state_only, a, nz, st);
   };
-  const char* what = tc ? "prefill_tc" : "prefill_simt";
-  const Plan pl = plan_split(s, tc);
+  const char* what = fam_name(fam);
+  const Plan pl = plan_split(s, fam != FAM_SIMT);
   if (pl.nseg > 1) {
     // two-phase split: local states of segments 0..nseg-2 (m-way sub-split), then every
     // segment seeded from them in its prologue; workspace from the library's stream pool
@@ -220,7 +252,7 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
         e = launch(q, o, s_in, s_out, false, b, (int)pl.nseg);
       }
       cudaFreeAsync(loc, st);
-      return cuda_status(e, tc ? "prefill_tc (sequence split)" : "prefill_simt (sequence split)");
+      return cuda_status(e, what);
     }
     cudaGetLastError();  // no workspace: run unsplit
   }
@@ -243,7 +275,7 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
   }
   // FFMA kernel (compute-bound, two or more CTAs per SM): the same schedule over the resident
   // slots whenever the units are not a whole number of waves
-  if (!tc && balance_env != 0) {
+  if (fam == FAM_SIMT && balance_env != 0) {
     const int slots = simt_balance_slots(q, k, v, s, dtype);
     const int64_t su = s.B * s.H * ceil_div(s.dv, 64);
     if (slots > 0 && su > slots && su % slots != 0) {
@@ -268,17 +300,14 @@ int linattn_state_pass(const void* k, const void* v, float* s_out, const float* 
   if (int e = check_dtype(dtype)) return e;
   if (!k || !v || !s_out || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
   cudaStream_t st = (cudaStream_t)stream;
-  const bool tc_ok = tc_supported(s, dtype) && aligned16({k, v});
-  if (kernel == LINATTN_KERNEL_TC && !tc_ok)
-    return fail(LINATTN_EUNSUPPORTED, "tensor-core state pass needs bf16, a supported shape and aligned tensors");
-  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_ok;
+  Fam fam;
+  if (int e = pick_family(s, dtype, kernel, {k, v}, fam)) return e;
   auto launch = [&](float* so, const SegArgs& a, int nz) {
-    return tc ? launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, so, s, true, a, nz, st)
-              : launch_prefill_simt(nullptr, k, v, nullptr, log2g, nullptr, so, s, dtype, true, a, nz, st);
+    return launch_fam(fam, nullptr, k, v, nullptr, log2g, nullptr, so, s, dtype, true, a, nz, st);
   };
   // few (b, h) units: every segment's local state in parallel (the split plan of the prefill,
   // all nseg segments here), then the end state = the state at N from them (one scan)
-  const Plan pl = plan_split(s, tc);
+  const Plan pl = plan_split(s, fam != FAM_SIMT);
   if (pl.nseg > 1) {
     const int64_t nloc = pl.nseg * pl.m;
     const size_t bytes = (size_t)nloc * s.B * s.H * s.dk * s.dv * sizeof(float);
@@ -292,11 +321,11 @@ int linattn_state_pass(const void* k, const void* v, float* s_out, const float* 
         e = launch_state_at(loc, nullptr, s_out, a, s.N, log2g, s, st);
       }
       cudaFreeAsync(loc, st);
-      return cuda_status(e, tc ? "state_pass_tc (split)" : "state_pass_simt (split)");
+      return cuda_status(e, fam_name(fam));
     }
     cudaGetLastError();
   }
-  return cuda_status(launch(s_out, SegArgs{}, 1), tc ? "state_pass_tc" : "state_pass_simt");
+  return cuda_status(launch(s_out, SegArgs{}, 1), fam_name(fam));
 }
 
 static int check_seg(const ShapeArgs& s, int64_t seg_len, int64_t m, bool tc) {
@@ -315,7 +344,9 @@ int linattn_seq_plan(int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv, in
   if (int e = check_dims(s, true)) return e;
   if (int e = check_dtype(dtype)) return e;
   if (!plan) return fail(LINATTN_EPARAM, "null plan pointer");
-  const Plan p = plan_split(s, kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype));
+  Fam fam;
+  if (int e = pick_family(s, dtype, kernel == LINATTN_KERNEL_AUTO ? LINATTN_KERNEL_AUTO : kernel, {}, fam)) return e;
+  const Plan p = plan_split(s, fam != FAM_SIMT);
   plan[0] = p.seg_len;
   plan[1] = p.nseg;
   plan[2] = p.m;
@@ -330,20 +361,16 @@ int linattn_state_pass_segmented(const void* k, const void* v, float* loc_out, c
   if (int e = check_dims(s, true)) return e;
   if (int e = check_dtype(dtype)) return e;
   if (!k || !v || !loc_out || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
-  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype) && aligned16({k, v});
-  if (kernel == LINATTN_KERNEL_TC && !tc)
-    return fail(LINATTN_EUNSUPPORTED, "tensor-core state pass needs bf16, a supported shape and aligned tensors");
-  if (int e = check_seg(s, seg_len, m, tc)) return e;
+  Fam fam;
+  if (int e = pick_family(s, dtype, kernel, {k, v}, fam)) return e;
+  if (int e = check_seg(s, seg_len, m, fam != FAM_SIMT)) return e;
   if (nseg < 1 || nseg > ceil_div(N, seg_len) || nseg * m > 65535)
     return fail(LINATTN_EPARAM, "segment count %lld outside [1, ceil(N/seg_len)=%lld]", (long long)nseg,
                 (long long)ceil_div(N, seg_len));
   const SegArgs a = make_seg(seg_len, m);
   cudaStream_t st = (cudaStream_t)stream;
-  if (tc)
-    return cuda_status(launch_prefill_tc(nullptr, k, v, nullptr, log2g, nullptr, loc_out, s, true, a,
-                                         (int)(nseg * m), st), "state_pass_tc (segmented)");
-  return cuda_status(launch_prefill_simt(nullptr, k, v, nullptr, log2g, nullptr, loc_out, s, dtype, true,
-                                         a, (int)(nseg * m), st), "state_pass_simt (segmented)");
+  return cuda_status(launch_fam(fam, nullptr, k, v, nullptr, log2g, nullptr, loc_out, s, dtype, true, a,
+                                (int)(nseg * m), st), fam_name(fam));
 }
 
 int linattn_prefill_segmented(const void* q, const void* k, const void* v, void* o, const float* log2g,
@@ -355,10 +382,9 @@ int linattn_prefill_segmented(const void* q, const void* k, const void* v, void*
   if (int e = check_dims(s, true)) return e;
   if (int e = check_dtype(dtype)) return e;
   if (!q || !k || !v || !o || !log2g) return fail(LINATTN_EPARAM, "null tensor pointer");
-  const bool tc = kernel != LINATTN_KERNEL_SIMT && tc_supported(s, dtype) && aligned16({q, k, v, o});
-  if (kernel == LINATTN_KERNEL_TC && !tc)
-    return fail(LINATTN_EUNSUPPORTED, "tensor-core prefill needs bf16, dk in {64,128,256}, dv %% 64 == 0, aligned");
-  if (int e = check_seg(s, seg_len, 1, tc)) return e;
+  Fam fam;
+  if (int e = pick_family(s, dtype, kernel, {q, k, v, o}, fam)) return e;
+  if (int e = check_seg(s, seg_len, 1, fam != FAM_SIMT)) return e;
   if (loc && (nloc < 0 || loc_seg_len < 1 || loc_m < 1 || nloc > ceil_div(N, loc_seg_len) * loc_m))
     return fail(LINATTN_EPARAM, "bad local-state geometry (seg_len %lld, m %lld, count %lld)",
                 (long long)loc_seg_len, (long long)loc_m, (long long)nloc);
@@ -370,11 +396,8 @@ int linattn_prefill_segmented(const void* q, const void* k, const void* v, void*
   attach_loc(a, loc, loc_seg_len, loc_m, nloc);
   a.loc_incl = loc_inclusive ? 1 : 0;
   cudaStream_t st = (cudaStream_t)stream;
-  if (tc)
-    return cuda_status(launch_prefill_tc(q, k, v, o, log2g, s_in, s_out, s, false, a, (int)nseg, st),
-                       "prefill_tc (segmented)");
-  return cuda_status(launch_prefill_simt(q, k, v, o, log2g, s_in, s_out, s, dtype, false, a, (int)nseg, st),
-                     "prefill_simt (segmented)");
+  return cuda_status(launch_fam(fam, q, k, v, o, log2g, s_in, s_out, s, dtype, false, a, (int)nseg, st),
+                     fam_name(fam));
 }
 
 int linattn_segment_prefix(const float* loc, int64_t loc_seg_len, int64_t loc_m, int64_t nloc, float* incl,
@@ -463,12 +486,17 @@ int linattn_release_workspace(void) {
 
 int linattn_prefill_kernel(int64_t dk, int64_t dv, int dtype) {
   ShapeArgs s{1, 1, 1, dk, dv};
-  return tc_supported(s, dtype) ? LINATTN_KERNEL_TC : LINATTN_KERNEL_SIMT;
+  return tc_supported(s, dtype) ? LINATTN_KERNEL_TC : tf32_supported(s, dtype) ? LINATTN_KERNEL_TF32
+                                                                             : LINATTN_KERNEL_SIMT;
 }
 
 // Debug hook (not part of the public header): record per-chunk clock64 timestamps of
 // CTA (0,0) of subsequent tensor-core launches into a device buffer of 16 x 4096 u64.
 __attribute__((visibility("default"))) void linattn_debug_set_trace(void* dev_buf) { set_trace(dev_buf); }
+// Debug hook: the 3xTF32 kernel's CTA (0,0,0) dumps first-chunk intermediates (36864 floats).
+__attribute__((visibility("default"))) void linattn_debug_set_tf32_dump(void* dev_buf) {
+  g_tf32_dump = static_cast<float*>(dev_buf);
+}
 
 const char* linattn_last_error(void) { return g_last_error.c_str(); }
 

@@ -179,6 +179,13 @@ cudaError_t launch_prefill_simt_balanced(const void* q, const void* k, const voi
                                          const ShapeArgs& s, int dtype, int slots, void* ws,
                                          cudaStream_t stream);
 
+// 3xTF32 tensor-core prefill (fp32 parity mode): fp32, dk <= 128, dk and dv multiples of 4,
+// 16-byte aligned tensors; cudaErrorNotSupported otherwise.  Same SegArgs / nz contract.
+bool tf32_supported(const ShapeArgs& s, int dtype);
+cudaError_t launch_prefill_tf32(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                                const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
+                                const SegArgs& sa, int nz, cudaStream_t stream);
+
 // Returns cudaErrorNotSupported when the shape is outside the TC kernel's envelope.
 cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void* o,
                               const float* log2g, const float* s_in, float* s_out,

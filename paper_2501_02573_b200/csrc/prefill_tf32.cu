@@ -1,0 +1,562 @@
+// K6: the fp32 parity mode on the tensor cores -- 3xTF32 chunked prefill (tcgen05 kind::tf32).
+//
+// Same algebra and transposed layout as the bf16 kernel (prefill_tc.cu, v2) -- every accumulator
+// has M = 128 TMEM lanes (lane = dv row d) -- with fp32 operands split into a tf32 "hi" part and a
+// "lo" remainder, x = hi + lo with hi = x with its low 13 mantissa bits cleared, so each product
+// a.b is computed as hi(a).hi(b) + hi(a).lo(b) + lo(a).hi(b) (the dropped lo.lo term is ~2^-22
+// relative): three tf32 MMAs per product, fp32 accumulation in TMEM.  One chunk of C = 32 tokens:
+//
+//   MMA1  P^T[s][t]  = sum_i K[s][i] Q[t][i]                  (M=128 [32 live], N=32, K=dk)  x3
+//   mask  P^T       *= gamma^(t-s) (t >= s) in fp32, split -> P^T hi | lo in smem
+//   prep  K'[s]      = gamma^(L-1-s) K[s] in fp32, split;  lo parts of Q, K, V
+//   MMA2  dS^T[d][i] = sum_s V[s][d] K'[s][i]                  (M=128, N=dk, K=32)          x3
+//         Oi^T[d][t] = sum_s V[s][d] P^T[s][t]                 (M=128, N=32, K=32)          x3
+//         Ox^T[d][t] = sum_i S^T[d][i] Q[t][i]                 (A = S^T hi|lo in TMEM)      x3
+//   state S <- gamma^L S + dS  (fp32 registers of 8 state warps; hi/lo published to TMEM)
+//   out   O[t][d] = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t]  (fp32) -> smem -> TMA bulk store
+//
+// Reference: kernels.py:139-166 (two-level block, chunk L <= C with 1-based t), accumulated in
+// fp32 and checked against the f64 oracle at 1e-4 (verify.py:14).  1xTF32 misses
+// that bar (6.2e-4 measured); 3xTF32 meets it with ~1e-6.
+//
+// Why C = 32: the state S^T needs a hi and a lo copy in TMEM as the A operand of Ox (2 x dk
+// columns), next to dS (dk), P^T, Oi and Ox (C each): 3 x 128 + 3 x 32 = 480 of 512 columns.
+//
+// Warp roles (448 threads): 0 P^T mask + split, 1-3 operand prep (lo parts, K'), 4-11 running
+// state + outputs, 12 TMA producer, 13 MMA issuer / TMEM owner.
+#include <cstdlib>
+#include <mutex>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+#ifndef TF32_TRUNC_INPLACE
+#define TF32_TRUNC_INPLACE 1   // also clear the low mantissa bits of the TMA-loaded hi operands
+#endif
+
+namespace linattn {
+
+PFN_cuTensorMapEncodeTiled_v12000 tf32_encode_fn();
+float* g_tf32_dump = nullptr;   // debug: first-chunk intermediates of CTA (0, 0, 0), see linattn_debug_set_tf32_dump
+
+namespace {
+
+using namespace sm100;
+
+namespace v4 {
+
+constexpr int kC = 32;           // tokens per chunk
+constexpr int kDVT = 128;        // dv rows per CTA (MMA M)
+constexpr int kThreads = 448;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t T_P = 0, T_OX = 32, T_O = 64, T_DS = 128, T_SHI = 256, T_SLO = 384;
+
+// Shared memory (1 KiB aligned).  Q/K/V tiles are TMA boxes of [32 rows][32 fp32] (4 KiB, 128-byte
+// swizzle), column blocks 4 KiB apart.  MMA1 reads K as a 128-row A operand (rows 32..127 are
+// don't-care), i.e. 12 KiB past the last K box: K is followed by V in the stage, Klo by Qlo.
+template <int DKP, int STAGES>
+struct Cfg {
+  static constexpr int KB = DKP / 32;
+  static constexpr int QK_BYTES = kC * DKP * 4;
+  static constexpr int V_BYTES = kC * kDVT * 4;
+  static constexpr int STAGE_BYTES = 2 * QK_BYTES + V_BYTES;     // Q | K | V
+  static constexpr int OFF_KLO = STAGES * STAGE_BYTES;             // derived, one chunk:
+  static constexpr int OFF_QLO = OFF_KLO + QK_BYTES;               //   Klo | Qlo | K'hi | K'lo | Vlo
+  static constexpr int OFF_KPH = OFF_QLO + QK_BYTES;
+  static constexpr int OFF_KPL = OFF_KPH + QK_BYTES;
+  static constexpr int OFF_VLO = OFF_KPL + QK_BYTES;
+  static constexpr int OFF_P = OFF_VLO + V_BYTES;                  // P^T hi | lo [32 s][32 t]
+  static constexpr int OFF_OT = OFF_P + 2 * 4096;                  // output tile [32 t][128 d]
+  static constexpr int OFF_POW = OFF_OT + V_BYTES;                 // gamma^n, n = 0..32
+  static constexpr int OFF_BAR = OFF_POW + 64 * 4;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  // the 128-row A operand of MMA1 reads 12 KiB past the last K box (K then V in the stage, Klo then Qlo)
+  static_assert((KB + 3) * 4096 <= QK_BYTES + V_BYTES && (KB + 3) * 4096 <= OFF_VLO - OFF_KLO, "A overread");
+};
+
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+template <int DKP, int STAGES, bool SO>
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                    const float* __restrict__ log2g, const float* __restrict__ s_in, float* __restrict__ s_out,
+                    int H, int N, int dk, int dv, const SegArgs sa, float* __restrict__ dump) {
+  using G = Cfg<DKP, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* empty = full + STAGES;
+  uint64_t* prepA = empty + STAGES;      // Klo, Qlo written (96 arrivals)
+  uint64_t* prepB = prepA + 1;           // K'hi, K'lo, Vlo written (96)
+  uint64_t* derA_free = prepB + 1;       // MMA1 + Ox done with Klo/Qlo (commit)
+  uint64_t* derB_free = derA_free + 1;   // dS + Oi done with K'/Vlo (commit)
+  uint64_t* mma1_bar = derB_free + 1;    // P^T in TMEM (commit)
+  uint64_t* mask_bar = mma1_bar + 1;     // P^T hi/lo in smem, TMEM copy read (32)
+  uint64_t* p_free = mask_bar + 1;       // Oi done with P^T hi/lo smem (commit)
+  uint64_t* mma_s_bar = p_free + 1;      // dS ready (commit)
+  uint64_t* ds_free = mma_s_bar + 1;     // dS read by the state warps (256)
+  uint64_t* st_full = ds_free + 1;       // S hi/lo published in TMEM (256)
+  uint64_t* mma_o_bar = st_full + 1;     // Oi + Ox done (commit)
+  uint64_t* o_free = mma_o_bar + 1;      // O / Ox drained (256)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
+  float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);
+  uint8_t* ot_smem = smem + G::OFF_OT;
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int bh = blockIdx.y;
+  const int j0 = blockIdx.x * kDVT;
+  int lo, hi;
+  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
+  const int nch = hi > lo ? (hi - lo + kC - 1) / kC : 0;
+  const size_t per_state = (size_t)gridDim.y * dk * dv;
+
+  if (warp == 12 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(prepA, 96);
+    mbar_init(prepB, 96);
+    mbar_init(derA_free, 1);
+    mbar_init(derB_free, 1);
+    mbar_init(mma1_bar, 1);
+    mbar_init(mask_bar, 32);
+    mbar_init(p_free, 1);
+    mbar_init(mma_s_bar, 1);
+    mbar_init(ds_free, 256);
+    mbar_init(st_full, 256);
+    mbar_init(mma_o_bar, 1);
+    mbar_init(o_free, 256);
+    fence_barrier_init();
+    if (!SO) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_o);
+    }
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+  }
+  if (warp == 13) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  pdl_wait();   // the prologue above overlapped the previous kernel's tail
+  const float lg = log2g[bh % H];
+  if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const bool dumping = dump != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  if (dumping && threadIdx.x <= kC) dump[threadIdx.x] = pw[threadIdx.x];
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ P^T mask + hi/lo split
+    if (!SO) {
+      const int srow = (int)lane;                     // TMEM lane = key row s of the chunk
+      uint8_t* ph = smem + G::OFF_P;
+      uint8_t* pl = ph + 4096;
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(mma1_bar, c & 1);
+        tc_fence_after();
+        float p[32];
+        tmem_ld32(tbase + T_P, p);
+        tmem_wait_ld();
+        if (dumping && c == 0)
+          for (int t = 0; t < 32; ++t) dump[64 + srow * 32 + t] = p[t];
+        if (c > 0) mbar_wait(p_free, (c - 1) & 1);    // Oi(c-1) has read the previous P^T
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 h4, l4;
+          float* hp = &h4.x;
+          float* lp = &l4.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int t = 4 * j + e;
+            const float x = t >= srow ? p[t] * pw[t >= srow ? t - srow : 0] : 0.f;
+            hp[e] = tf32_hi(x);
+            lp[e] = x - hp[e];
+          }
+          const int off = srow * 128 + (((((j >> 1) ^ (srow & 3)) << 1) | (j & 1)) << 4);   // MN-major tf32
+          *reinterpret_cast<float4*>(ph + off) = h4;
+          *reinterpret_cast<float4*>(pl + off) = l4;
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(mask_bar);
+      }
+    }
+  } else if (warp < 4) {
+    // ------------------------------------------------------------ operand prep (96 threads)
+    const int pt = (int)threadIdx.x - 32;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % STAGES;
+      const int L = min(kC, hi - lo - c * kC);
+      uint8_t* st = smem + s * G::STAGE_BYTES;
+      uint8_t* qs = st;
+      uint8_t* ks = st + G::QK_BYTES;
+      uint8_t* vs = st + 2 * G::QK_BYTES;
+      mbar_wait(&full[s], (c / STAGES) & 1);
+      if (!SO) {
+        if (c > 0) mbar_wait(derA_free, (c - 1) & 1);
+        // Klo, Qlo (and, with TF32_TRUNC_INPLACE, the hi parts truncated in place)
+        for (int i = pt; i < 2 * G::QK_BYTES / 16; i += 96) {
+          const bool isk = i < G::QK_BYTES / 16;
+          const int o = (isk ? i : i - G::QK_BYTES / 16) * 16;
+          float4* src = reinterpret_cast<float4*>((isk ? ks : qs) + o);
+          float4* dst = reinterpret_cast<float4*>(smem + (isk ? G::OFF_KLO : G::OFF_QLO) + o);
+          float4 x = *src, h, l;
+          h.x = tf32_hi(x.x); h.y = tf32_hi(x.y); h.z = tf32_hi(x.z); h.w = tf32_hi(x.w);
+          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+          *dst = l;
+          if (TF32_TRUNC_INPLACE) *src = h;
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(prepA);
+      }
+      if (c > 0) mbar_wait(derB_free, (c - 1) & 1);
+      // Row units (a 128-byte row of one 32-column box): K' = gamma^(L-1-s) K (zero past the ragged
+      // end) split into hi | lo, and V split into hi (in place) | lo -- both re-laid from the TMA's
+      // 128B swizzle (16-byte chunk j of row r at j ^ (r & 7)) to the MN-major tf32 layout
+      // (32-byte granule g at g ^ (r & 3)), the only MN-major layout kind::tf32 reads.
+      for (int u = pt; u < (G::KB + 4) * kC; u += 96) {
+        const bool isv = u >= G::KB * kC;
+        const int uu = isv ? u - G::KB * kC : u;
+        const int r = uu & (kC - 1);
+        const int boff = (uu >> 5) * 4096 + r * 128;
+        const uint8_t* src = (isv ? vs : ks) + boff;
+        float4 x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = *reinterpret_cast<const float4*>(src + ((j ^ (r & 7)) << 4));
+        float w = 1.f;
+        if (!isv) {
+          w = r < L ? pw[r < L ? L - 1 - r : 0] : 0.f;
+          if (!SO && TF32_TRUNC_INPLACE) {   // K was truncated in place: K = hi + lo exactly
+            const uint8_t* ls = smem + G::OFF_KLO + boff;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 l = *reinterpret_cast<const float4*>(ls + ((j ^ (r & 7)) << 4));
+              x[j].x += l.x; x[j].y += l.y; x[j].z += l.z; x[j].w += l.w;
+            }
+          }
+        }
+        uint8_t* dh = isv ? (TF32_TRUNC_INPLACE ? vs + boff : nullptr) : smem + G::OFF_KPH + boff;
+        uint8_t* dl = smem + (isv ? G::OFF_VLO : G::OFF_KPL) + boff;
+        if (isv && !TF32_TRUNC_INPLACE) {   // V keeps its raw bits as hi: only the relayout
+          dh = vs + boff;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 v4 = x[j], h, l;
+          v4.x *= w; v4.y *= w; v4.z *= w; v4.w *= w;
+          h.x = tf32_hi(v4.x); h.y = tf32_hi(v4.y); h.z = tf32_hi(v4.z); h.w = tf32_hi(v4.w);
+          l.x = v4.x - h.x; l.y = v4.y - h.y; l.z = v4.z - h.z; l.w = v4.w - h.w;
+          const int pos = ((((j >> 1) ^ (r & 3)) << 1) | (j & 1)) << 4;
+          *reinterpret_cast<float4*>(dh + pos) = (isv && !TF32_TRUNC_INPLACE) ? v4 : h;
+          *reinterpret_cast<float4*>(dl + pos) = l;
+        }
+      }
+      fence_proxy_async_smem();
+      if (dumping && c == 0) {   // raw smem of K, V (stage 0), K'hi, Vlo after prep: 4 x 4096 floats
+        named_bar_sync(3, 96);
+        for (int i = pt; i < 4096; i += 96) {
+          dump[20480 + i] = i < G::QK_BYTES / 4 ? reinterpret_cast<const float*>(ks)[i] : 0.f;
+          dump[24576 + i] = reinterpret_cast<const float*>(vs)[i];
+          dump[28672 + i] = i < G::QK_BYTES / 4 ? reinterpret_cast<const float*>(smem + G::OFF_KPH)[i] : 0.f;
+          dump[32768 + i] = reinterpret_cast<const float*>(smem + G::OFF_VLO)[i];
+        }
+      }
+      mbar_arrive(prepB);
+    }
+  } else if (warp < 12) {
+    // ------------------------------------------------------------ running state + outputs
+    // warp (g, sub): TMEM lanes sub*32.. (dv rows d), state columns [g*SC, (g+1)*SC),
+    // output tokens [g*16, g*16+16) of each chunk.
+    constexpr int SC = DKP / 2;
+    const int g = (warp - 4) / 4;
+    const int sub = (warp - 4) % 4;
+    const int d = sub * 32 + (int)lane;
+    const int col0 = g * SC;
+    const int jd = j0 + d;
+    const bool dv_ok = jd < dv;
+    const uint32_t lane_base = tbase + ((uint32_t)(sub * 32) << 16);
+    const bool leader = warp == 4 && lane == 0;
+    float S[SC];
+    auto publish = [&]() {
+#pragma unroll
+      for (int j = 0; j < SC / 8; ++j) {
+        uint32_t hv[8], lv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float h = tf32_hi(S[8 * j + i]);
+          hv[i] = __float_as_uint(h);
+          lv[i] = __float_as_uint(S[8 * j + i] - h);
+        }
+        tmem_st8(lane_base + T_SHI + col0 + 8 * j, hv);
+        tmem_st8(lane_base + T_SLO + col0 + 8 * j, lv);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(st_full);
+    };
+    // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs), 16 columns at a time
+    {
+      const float w_in = gpow(lg, (float)lo);
+      const bool in_ok = s_in != nullptr && dv_ok;
+#pragma unroll
+      for (int j = 0; j < SC; j += 16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int ci = col0 + j + i;
+          S[j + i] = (in_ok && ci < dk) ? w_in * __ldg(s_in + ((size_t)bh * dk + ci) * dv + jd) : 0.f;
+        }
+        for (int qi = 0; qi < sa.nloc; ++qi) {
+          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
+          if (wq < 0.f || !dv_ok) continue;
+          const float* lq = sa.loc + qi * per_state + ((size_t)bh * dk + col0 + j) * dv + jd;
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (col0 + j + i < dk) S[j + i] = fmaf(wq, __ldg(lq + (size_t)i * dv), S[j + i]);
+        }
+      }
+    }
+    if (!SO && nch > 0) publish();
+    for (int c = 0; c < nch; ++c) {
+      const int L = min(kC, hi - lo - c * kC);
+      mbar_wait(mma_s_bar, c & 1);
+      tc_fence_after();
+      const float carry = pw[L];
+#pragma unroll
+      for (int j = 0; j < SC / 16; ++j) {
+        float ds[16];
+        tmem_ld16(lane_base + T_DS + col0 + 16 * j, ds);
+        tmem_wait_ld();
+        if (dumping && c == 0)
+          for (int i = 0; i < 16; ++i) dump[2048 + d * 128 + col0 + 16 * j + i] = ds[i];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) S[16 * j + i] = fmaf(carry, S[16 * j + i], ds[i]);
+      }
+      tc_fence_before();
+      mbar_arrive(ds_free);
+      if (SO) continue;
+      mbar_wait(mma_o_bar, c & 1);                 // Oi, Ox done: S hi/lo may be replaced
+      tc_fence_after();
+      if (c != nch - 1) publish();
+      // ---- outputs: O[t][d] = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t], tokens g*16 .. g*16+15
+      float o[16], x[16];
+      tmem_ld16(lane_base + T_O + g * 16, o);
+      tmem_ld16(lane_base + T_OX + g * 16, x);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(o_free);
+      if (leader) bulk_wait_read<0>();             // the previous chunk's store has read the tile
+      named_bar_sync(1, 256);
+      uint8_t* box = ot_smem + sub * 4096;         // d-block sub: [32 t][32 d] fp32, 128B swizzle
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int t = g * 16 + i;
+        const float val = fmaf(pw[t + 1], x[i], o[i]);
+        *reinterpret_cast<float*>(box + t * 128 + (((lane >> 2) ^ (t & 7)) << 4) + (lane & 3) * 4) = val;
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(2, 256);
+      if (leader) {
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) tma_store_3d(&tm_o, ot_smem + nb * 4096, j0 + nb * 32, lo + c * kC, bh);
+        bulk_commit();
+      }
+    }
+    // end state: state-only launches write one local state per segment, full launches only the
+    // segment ending the sequence (its seed already covers every earlier token)
+    if (s_out && dv_ok && (SO || blockIdx.z == gridDim.z - 1)) {
+      float* so = s_out + (SO ? blockIdx.z * per_state : 0) + (size_t)bh * dk * dv + jd;
+#pragma unroll
+      for (int i = 0; i < SC; ++i)
+        if (col0 + i < dk) so[(size_t)(col0 + i) * dv] = S[i];
+    }
+    if (leader) bulk_wait<0>();
+  } else if (warp == 12) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint32_t bytes = (SO ? 0 : G::QK_BYTES) + G::QK_BYTES + G::V_BYTES;
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % STAGES;
+        const int t0 = lo + c * kC;
+        mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * G::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[s], bytes);
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb) {
+          if (!SO) tma_load_3d(st + kb * 4096, &tm_q, &full[s], kb * 32, t0, bh);
+          tma_load_3d(st + G::QK_BYTES + kb * 4096, &tm_k, &full[s], kb * 32, t0, bh);
+        }
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+          tma_load_3d(st + 2 * G::QK_BYTES + nb * 4096, &tm_v, &full[s], j0 + nb * 32, t0, bh);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ MMA issuer (whole warp)
+    constexpr uint32_t id_qk = idesc_tf32(128, kC, false, false);    // P^T = K Q^T
+    constexpr uint32_t id_vk = idesc_tf32(128, DKP, true, true);     // dS^T = V^T K'
+    constexpr uint32_t id_vp = idesc_tf32(128, kC, true, true);      // Oi^T = V^T P^T
+    constexpr uint32_t id_sq = idesc_tf32(128, kC, false, false);    // Ox^T = S^T(TMEM) Q^T
+    const uint32_t base = smem_u32(smem);
+    const uint64_t dK0 = smem_desc_sw128(base, 16, 1024);             // K-major
+    const uint64_t dM0 = smem_desc_sw128_b32(base, 4096, 512);        // MN-major tf32, 32-wide blocks
+    constexpr uint64_t kStage = G::STAGE_BYTES >> 4, kQK = G::QK_BYTES >> 4;
+    const uint64_t klo_k = dK0 + (G::OFF_KLO >> 4), qlo_k = dK0 + (G::OFF_QLO >> 4);
+    const uint64_t kph_m = dM0 + (G::OFF_KPH >> 4), kpl_m = dM0 + (G::OFF_KPL >> 4);
+    const uint64_t vlo_m = dM0 + (G::OFF_VLO >> 4);
+    const uint64_t ph_m = dM0 + (G::OFF_P >> 4), pl_m = ph_m + (4096 >> 4);
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % STAGES;
+      const uint64_t q_k = dK0 + s * kStage, k_k = q_k + kQK;         // raw Q, K (hi), K-major
+      const uint64_t v_m = dM0 + s * kStage + 2 * kQK;                // raw V (hi), MN-major
+      mbar_wait(&full[s], (c / STAGES) & 1);
+      if (!SO) {
+        mbar_wait(prepA, c & 1);
+        tc_fence_after();
+        // P^T = Khi Qhi + Khi Qlo + Klo Qhi
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t o = kb * 256 + kk * 2;
+            mma_tf32_ss_elect(tbase + T_P, k_k + o, q_k + o, id_qk, (kb | kk) != 0);
+            mma_tf32_ss_elect(tbase + T_P, k_k + o, qlo_k + o, id_qk, 1);
+            mma_tf32_ss_elect(tbase + T_P, klo_k + o, q_k + o, id_qk, 1);
+          }
+        mma_commit_elect(mma1_bar);
+      }
+      mbar_wait(prepB, c & 1);
+      if (c > 0) mbar_wait(ds_free, (c - 1) & 1);
+      tc_fence_after();
+      // dS^T = Vhi K'hi + Vhi K'lo + Vlo K'hi   (K step = 8 token rows = 1 KiB)
+#pragma unroll
+      for (int ks = 0; ks < kC / 8; ++ks) {
+        const uint64_t o = ks * 64;
+        mma_tf32_ss_elect(tbase + T_DS, v_m + o, kph_m + o, id_vk, ks != 0);
+        mma_tf32_ss_elect(tbase + T_DS, v_m + o, kpl_m + o, id_vk, 1);
+        mma_tf32_ss_elect(tbase + T_DS, vlo_m + o, kph_m + o, id_vk, 1);
+      }
+      mma_commit_elect(mma_s_bar);
+      if (!SO) {
+        mbar_wait(mask_bar, c & 1);
+        if (c > 0) mbar_wait(o_free, (c - 1) & 1);
+        tc_fence_after();
+        // Oi^T = Vhi Phi + Vhi Plo + Vlo Phi
+#pragma unroll
+        for (int ks = 0; ks < kC / 8; ++ks) {
+          const uint64_t o = ks * 64;
+          mma_tf32_ss_elect(tbase + T_O, v_m + o, ph_m + o, id_vp, ks != 0);
+          mma_tf32_ss_elect(tbase + T_O, v_m + o, pl_m + o, id_vp, 1);
+          mma_tf32_ss_elect(tbase + T_O, vlo_m + o, ph_m + o, id_vp, 1);
+        }
+        mma_commit_elect(p_free);
+        mma_commit_elect(derB_free);
+        mbar_wait(st_full, c & 1);
+        tc_fence_after();
+        // Ox^T = Shi Qhi + Shi Qlo + Slo Qhi   (A from TMEM: 8 columns per K step)
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t o = kb * 256 + kk * 2;
+            const uint32_t col = (kb * 4 + kk) * 8;
+            mma_tf32_ts_elect(tbase + T_OX, tbase + T_SHI + col, q_k + o, id_sq, (kb | kk) != 0);
+            mma_tf32_ts_elect(tbase + T_OX, tbase + T_SHI + col, qlo_k + o, id_sq, 1);
+            mma_tf32_ts_elect(tbase + T_OX, tbase + T_SLO + col, q_k + o, id_sq, 1);
+          }
+        mma_commit_elect(mma_o_bar);
+        mma_commit_elect(derA_free);
+      } else {
+        mma_commit_elect(derB_free);
+      }
+      mma_commit_elect(&empty[s]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 13) tmem_dealloc<kTmemCols>(tbase);
+}
+
+}  // namespace v4
+
+// [BH][N][D] fp32 viewed as a 3-D tensor (D fastest); boxes of 32 x 32, 128B swizzle.
+bool make_map_f32(CUtensorMap* map, const void* base, int64_t D, int64_t N, int64_t BH) {
+  auto fn = tf32_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)N, (cuuint64_t)BH};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 4, (cuuint64_t)(N * D * 4)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int DKP, int STAGES, bool SO>
+cudaError_t launch_v4(const void* q, const void* k, const void* v, void* o, const float* log2g, const float* s_in,
+                      float* s_out, const ShapeArgs& s, const SegArgs& sa, int nz, cudaStream_t stream) {
+  using G = v4::Cfg<DKP, STAGES>;
+  static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
+  const int64_t BH = s.B * s.H;
+  CUtensorMap mq, mk, mv, mo;
+  if (!make_map_f32(&mk, k, s.dk, s.N, BH) || !make_map_f32(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
+  mq = mk;
+  mo = mv;
+  if (!SO && (!make_map_f32(&mq, q, s.dk, s.N, BH) || !make_map_f32(&mo, o, s.dv, s.N, BH)))
+    return cudaErrorInvalidValue;
+  auto kern = v4::prefill_tf32_kernel<DKP, STAGES, SO>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  if (err != cudaSuccess) return err;
+  const dim3 grid((unsigned)((s.dv + v4::kDVT - 1) / v4::kDVT), (unsigned)BH, (unsigned)nz);
+  err = launch_pdl(kern, grid, dim3(v4::kThreads), G::SMEM, stream, mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H,
+                   (int)s.N, (int)s.dk, (int)s.dv, sa, g_tf32_dump);
+  if (err != cudaSuccess) return err;
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+PFN_cuTensorMapEncodeTiled_v12000 tf32_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool tf32_supported(const ShapeArgs& s, int dtype) {
+  if (dtype != LINATTN_F32) return false;
+  if (s.dk < 1 || s.dk > 128 || s.dk % 4 != 0 || s.dv % 4 != 0) return false;   // TMA: 16-byte rows
+  return tf32_encode_fn() != nullptr;
+}
+
+cudaError_t launch_prefill_tf32(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                                const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
+                                const SegArgs& sa, int nz, cudaStream_t stream) {
+  for (const void* p : {q, k, v, (const void*)o})
+    if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return cudaErrorNotSupported;
+  if (!tf32_supported(s, LINATTN_F32)) return cudaErrorNotSupported;
+  if (s.dk <= 32)
+    return state_only ? launch_v4<32, 6, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
+                      : launch_v4<32, 6, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
+  if (s.dk <= 64)
+    return state_only ? launch_v4<64, 4, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
+                      : launch_v4<64, 4, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
+  return state_only ? launch_v4<128, 2, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
+                    : launch_v4<128, 2, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
+}
+
+}  // namespace linattn

@@ -302,7 +302,7 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
             ops_count = inputs.batch * inputs.heads * inputs.seqlen * inputs.rank * inputs.dim * (
                 3 if inputs.decay else 2)  # reference row-based count (kernels.py:105)
         else:
-            kernel = "simt" if method is MethodId.B200_CHUNKED_F32 else "auto"
+            kernel = "auto"
             split = max(1, int(params.seq_parts)) if method is MethodId.B200_SEQPAR else None
             run = lambda q, k, v, l2, o: ops.prefill(q, k, v, l2, out=o, kernel=kernel, seq_split=split)  # noqa: E731
             chunk = SIMT_CHUNK if method is MethodId.B200_CHUNKED_F32 else TC_CHUNK
@@ -319,7 +319,7 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
         out_dev = ops.prefill(q, k, v, log2g, kernel="auto")
         chunk = TC_CHUNK
     elif method is MethodId.B200_CHUNKED_F32:
-        out_dev = ops.prefill(q, k, v, log2g, kernel="simt")
+        out_dev = ops.prefill(q, k, v, log2g, kernel="auto")
         chunk = SIMT_CHUNK
     elif method is MethodId.B200_SEQPAR:
         out_dev = _seqpar(q, k, v, log2g, max(1, int(params.seq_parts)), "auto")

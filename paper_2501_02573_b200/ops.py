@@ -19,7 +19,7 @@ from . import _lib
 from .errors import LinAttnError, ShapeError, UsageError
 
 _DTYPES = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}
-_KERNELS = {"auto": _lib.KERNEL_AUTO, "tc": _lib.KERNEL_TC, "simt": _lib.KERNEL_SIMT}
+_KERNELS = {"auto": _lib.KERNEL_AUTO, "tc": _lib.KERNEL_TC, "simt": _lib.KERNEL_SIMT, "tf32": _lib.KERNEL_TF32}
 
 
 def _require_cuda(*ts):
@@ -342,11 +342,12 @@ def recurrent(q, k, v, log2g, *, s_in=None, s_out=None, out=None):
 
 
 def prefill_kernel_name(dk: int, dv: int, dtype=torch.bfloat16, kernel: str = "auto") -> str:
-    """Which kernel family a prefill of this shape runs ("prefill_tc" or "prefill_simt")."""
-    if kernel == "simt":
-        return "prefill_simt"
+    """Which kernel family a prefill of this shape runs: "prefill_tc" (tcgen05 bf16),
+    "prefill_tf32" (tcgen05 3xTF32, the fp32 parity mode) or "prefill_simt" (FFMA)."""
+    if kernel != "auto":
+        return {"tc": "prefill_tc", "tf32": "prefill_tf32", "simt": "prefill_simt"}[kernel]
     code = _lib.load().linattn_prefill_kernel(dk, dv, _DTYPES[dtype])
-    return "prefill_tc" if code == _lib.KERNEL_TC else "prefill_simt"
+    return {_lib.KERNEL_TC: "prefill_tc", _lib.KERNEL_TF32: "prefill_tf32"}.get(code, "prefill_simt")
 
 
 def chunked_opcount(batch: int, heads: int, n: int, r: int, d: int, decay: bool, chunk: int) -> int:
