@@ -22,8 +22,14 @@
 // Why C = 32: the state S^T needs a hi and a lo copy in TMEM as the A operand of Ox (2 x dk
 // columns), next to dS (dk), P^T, Oi and Ox (C each): 3 x 128 + 3 x 32 = 480 of 512 columns.
 //
-// Warp roles (448 threads): 0 P^T mask + split, 1-3 operand prep (lo parts, K'), 4-11 running
-// state + outputs, 12 TMA producer, 13 MMA issuer / TMEM owner.
+// MMA1 runs at M = 64 (rows 0-15 of the chunk land in TMEM lanes 0-15, rows 16-31 in lanes
+// 32-47), halving the shared-memory reads of its A operand; the lo parts of Q and K are double
+// buffered so the next chunk's operand prep overlaps this chunk's MMAs, and the tensor pipe
+// issues MMA1 of chunk c+1 ahead of O_inter of chunk c.
+//
+// Warp roles (512 threads): 0-1 P^T mask + split (16 key rows each), 2-3 and 14-15 operand prep
+// (lo parts, K', MN-major relayout), 4-11 running state + outputs (direct coalesced fp32 stores),
+// 12 TMA producer, 13 MMA issuer / TMEM owner.
 #include <cstdlib>
 #include <mutex>
 #include <cudaTypedefs.h>
@@ -32,7 +38,8 @@
 #include "sm100.cuh"
 
 #ifndef TF32_TRUNC_INPLACE
-#define TF32_TRUNC_INPLACE 1   // also clear the low mantissa bits of the TMA-loaded hi operands
+#define TF32_TRUNC_INPLACE 0   // 1: also clear the low mantissa bits of the TMA-loaded hi operands (the
+                               // MMA ignores them: bit-identical results measured on B200, so off)
 #endif
 
 namespace linattn {
@@ -48,7 +55,8 @@ namespace v4 {
 
 constexpr int kC = 32;           // tokens per chunk
 constexpr int kDVT = 128;        // dv rows per CTA (MMA M)
-constexpr int kThreads = 448;
+constexpr int kThreads = 512;
+constexpr int kPrep = 128;       // operand-prep threads (warps 2, 3, 14, 15)
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t T_P = 0, T_OX = 32, T_O = 64, T_DS = 128, T_SHI = 256, T_SLO = 384;
 
@@ -61,18 +69,16 @@ struct Cfg {
   static constexpr int QK_BYTES = kC * DKP * 4;
   static constexpr int V_BYTES = kC * kDVT * 4;
   static constexpr int STAGE_BYTES = 2 * QK_BYTES + V_BYTES;     // Q | K | V
-  static constexpr int OFF_KLO = STAGES * STAGE_BYTES;             // derived, one chunk:
-  static constexpr int OFF_QLO = OFF_KLO + QK_BYTES;               //   Klo | Qlo | K'hi | K'lo | Vlo
-  static constexpr int OFF_KPH = OFF_QLO + QK_BYTES;
+  static constexpr int OFF_KLO = STAGES * STAGE_BYTES;             // [2] x (Klo | Qlo), K-major
+  static constexpr int OFF_KPH = OFF_KLO + 4 * QK_BYTES;           // K'hi | K'lo | Vlo, MN-major
   static constexpr int OFF_KPL = OFF_KPH + QK_BYTES;
   static constexpr int OFF_VLO = OFF_KPL + QK_BYTES;
   static constexpr int OFF_P = OFF_VLO + V_BYTES;                  // P^T hi | lo [32 s][32 t]
-  static constexpr int OFF_OT = OFF_P + 2 * 4096;                  // output tile [32 t][128 d]
-  static constexpr int OFF_POW = OFF_OT + V_BYTES;                 // gamma^n, n = 0..32
+  static constexpr int OFF_POW = OFF_P + 2 * 4096;                 // gamma^n, n = 0..32
   static constexpr int OFF_BAR = OFF_POW + 64 * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  // the 128-row A operand of MMA1 reads 12 KiB past the last K box (K then V in the stage, Klo then Qlo)
-  static_assert((KB + 3) * 4096 <= QK_BYTES + V_BYTES && (KB + 3) * 4096 <= OFF_VLO - OFF_KLO, "A overread");
+  // the 64-row A operand of MMA1 reads 4 KiB past the last K box (K then V in the stage, Klo then Qlo)
+  static_assert((KB + 1) * 4096 <= QK_BYTES + V_BYTES && (KB + 1) * 4096 <= 2 * QK_BYTES, "A overread");
 };
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
@@ -80,20 +86,22 @@ __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__flo
 template <int DKP, int STAGES, bool SO>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                    const __grid_constant__ CUtensorMap tm_v, float* __restrict__ o,
                     const float* __restrict__ log2g, const float* __restrict__ s_in, float* __restrict__ s_out,
                     int H, int N, int dk, int dv, const SegArgs sa, float* __restrict__ dump) {
   using G = Cfg<DKP, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // aligned by pointer arithmetic (not via an integer cast) so ptxas keeps the shared address
+  // space: LDS/STS instead of generic loads/stores
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   uint64_t* empty = full + STAGES;
-  uint64_t* prepA = empty + STAGES;      // Klo, Qlo written (96 arrivals)
-  uint64_t* prepB = prepA + 1;           // K'hi, K'lo, Vlo written (96)
-  uint64_t* derA_free = prepB + 1;       // MMA1 + Ox done with Klo/Qlo (commit)
-  uint64_t* derB_free = derA_free + 1;   // dS + Oi done with K'/Vlo (commit)
+  uint64_t* prepA = empty + STAGES;      // [2] Klo, Qlo of buffer b written (128 arrivals)
+  uint64_t* derA_free = prepA + 2;       // [2] MMA1 + Ox done with buffer b (commit)
+  uint64_t* prepB = derA_free + 2;       // K'hi, K'lo, Vlo written (128)
+  uint64_t* derB_free = prepB + 1;       // dS + Oi done with K'/Vlo (commit)
   uint64_t* mma1_bar = derB_free + 1;    // P^T in TMEM (commit)
-  uint64_t* mask_bar = mma1_bar + 1;     // P^T hi/lo in smem, TMEM copy read (32)
+  uint64_t* mask_bar = mma1_bar + 1;     // P^T hi/lo in smem, TMEM copy read (64)
   uint64_t* p_free = mask_bar + 1;       // Oi done with P^T hi/lo smem (commit)
   uint64_t* mma_s_bar = p_free + 1;      // dS ready (commit)
   uint64_t* ds_free = mma_s_bar + 1;     // dS read by the state warps (256)
@@ -102,7 +110,6 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   uint64_t* o_free = mma_o_bar + 1;      // O / Ox drained (256)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
   float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);
-  uint8_t* ot_smem = smem + G::OFF_OT;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -118,12 +125,14 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(prepA, 96);
-    mbar_init(prepB, 96);
-    mbar_init(derA_free, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&prepA[b], kPrep);
+      mbar_init(&derA_free[b], 1);
+    }
+    mbar_init(prepB, kPrep);
     mbar_init(derB_free, 1);
     mbar_init(mma1_bar, 1);
-    mbar_init(mask_bar, 32);
+    mbar_init(mask_bar, 64);
     mbar_init(p_free, 1);
     mbar_init(mma_s_bar, 1);
     mbar_init(ds_free, 256);
@@ -131,10 +140,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     mbar_init(mma_o_bar, 1);
     mbar_init(o_free, 256);
     fence_barrier_init();
-    if (!SO) {
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_o);
-    }
+    if (!SO) tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
   }
@@ -150,61 +156,74 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   const bool dumping = dump != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
   if (dumping && threadIdx.x <= kC) dump[threadIdx.x] = pw[threadIdx.x];
 
-  if (warp == 0) {
+  if (warp < 2) {
     // ------------------------------------------------------------ P^T mask + hi/lo split
+    // M = 64 accumulator: key row s = 16 * warp + lane (lanes 0-15 of subpartitions 0 and 1)
     if (!SO) {
-      const int srow = (int)lane;                     // TMEM lane = key row s of the chunk
+      const int srow = 16 * (int)warp + (int)(lane & 15);
+      const bool live = lane < 16;
       uint8_t* ph = smem + G::OFF_P;
       uint8_t* pl = ph + 4096;
       for (int c = 0; c < nch; ++c) {
         mbar_wait(mma1_bar, c & 1);
         tc_fence_after();
         float p[32];
-        tmem_ld32(tbase + T_P, p);
+        tmem_ld32(tbase + ((32 * warp) << 16) + T_P, p);
         tmem_wait_ld();
-        if (dumping && c == 0)
+        if (dumping && c == 0 && live)
           for (int t = 0; t < 32; ++t) dump[64 + srow * 32 + t] = p[t];
         if (c > 0) mbar_wait(p_free, (c - 1) & 1);    // Oi(c-1) has read the previous P^T
+        if (live) {
+          float hv[32], lv[32];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 h4, l4;
-          float* hp = &h4.x;
-          float* lp = &l4.x;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int t = 4 * j + e;
+          for (int t = 0; t < 32; ++t) {
             const float x = t >= srow ? p[t] * pw[t >= srow ? t - srow : 0] : 0.f;
-            hp[e] = tf32_hi(x);
-            lp[e] = x - hp[e];
+            hv[t] = tf32_hi(x);
+            lv[t] = x - hv[t];
           }
-          const int off = srow * 128 + (((((j >> 1) ^ (srow & 3)) << 1) | (j & 1)) << 4);   // MN-major tf32
-          *reinterpret_cast<float4*>(ph + off) = h4;
-          *reinterpret_cast<float4*>(pl + off) = l4;
+          // MN-major tf32 layout: 16-byte piece j of row s at granule (j/2) ^ (s & 3), half j & 1.
+          // Rows s and s+4 share granule positions, so they store the two halves in opposite
+          // order (jj ^ flip) and a quarter-warp never hits one bank twice.
+          const int flip = (srow >> 2) & 1;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int j = jj ^ flip;
+            const int off = srow * 128 + (((((j >> 1) ^ (srow & 3)) << 1) | (j & 1)) << 4);
+            const float4 h4 = flip ? make_float4(hv[4 * (jj ^ 1)], hv[4 * (jj ^ 1) + 1], hv[4 * (jj ^ 1) + 2], hv[4 * (jj ^ 1) + 3])
+                                   : make_float4(hv[4 * jj], hv[4 * jj + 1], hv[4 * jj + 2], hv[4 * jj + 3]);
+            const float4 l4 = flip ? make_float4(lv[4 * (jj ^ 1)], lv[4 * (jj ^ 1) + 1], lv[4 * (jj ^ 1) + 2], lv[4 * (jj ^ 1) + 3])
+                                   : make_float4(lv[4 * jj], lv[4 * jj + 1], lv[4 * jj + 2], lv[4 * jj + 3]);
+            *reinterpret_cast<float4*>(ph + off) = h4;
+            *reinterpret_cast<float4*>(pl + off) = l4;
+          }
         }
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(mask_bar);
       }
     }
-  } else if (warp < 4) {
-    // ------------------------------------------------------------ operand prep (96 threads)
-    const int pt = (int)threadIdx.x - 32;
+  } else if (warp < 4 || warp >= 14) {
+    // ------------------------------------------------------------ operand prep (128 threads)
+    const int pt = warp < 4 ? (int)threadIdx.x - 64 : (int)threadIdx.x - 384;
     for (int c = 0; c < nch; ++c) {
       const int s = c % STAGES;
+      const int b = c & 1;
       const int L = min(kC, hi - lo - c * kC);
       uint8_t* st = smem + s * G::STAGE_BYTES;
       uint8_t* qs = st;
       uint8_t* ks = st + G::QK_BYTES;
       uint8_t* vs = st + 2 * G::QK_BYTES;
+      uint8_t* klo = smem + G::OFF_KLO + b * 2 * G::QK_BYTES;
+      uint8_t* qlo = klo + G::QK_BYTES;
       mbar_wait(&full[s], (c / STAGES) & 1);
       if (!SO) {
-        if (c > 0) mbar_wait(derA_free, (c - 1) & 1);
+        if (c >= 2) mbar_wait(&derA_free[b], ((c >> 1) - 1) & 1);
         // Klo, Qlo (and, with TF32_TRUNC_INPLACE, the hi parts truncated in place)
-        for (int i = pt; i < 2 * G::QK_BYTES / 16; i += 96) {
+        for (int i = pt; i < 2 * G::QK_BYTES / 16; i += kPrep) {
           const bool isk = i < G::QK_BYTES / 16;
-          const int o = (isk ? i : i - G::QK_BYTES / 16) * 16;
-          float4* src = reinterpret_cast<float4*>((isk ? ks : qs) + o);
-          float4* dst = reinterpret_cast<float4*>(smem + (isk ? G::OFF_KLO : G::OFF_QLO) + o);
+          const int off = (isk ? i : i - G::QK_BYTES / 16) * 16;
+          float4* src = reinterpret_cast<float4*>((isk ? ks : qs) + off);
+          float4* dst = reinterpret_cast<float4*>((isk ? klo : qlo) + off);
           float4 x = *src, h, l;
           h.x = tf32_hi(x.x); h.y = tf32_hi(x.y); h.z = tf32_hi(x.z); h.w = tf32_hi(x.w);
           l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
@@ -212,14 +231,18 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           if (TF32_TRUNC_INPLACE) *src = h;
         }
         fence_proxy_async_smem();
-        mbar_arrive(prepA);
+        mbar_arrive(&prepA[b]);
       }
       if (c > 0) mbar_wait(derB_free, (c - 1) & 1);
       // Row units (a 128-byte row of one 32-column box): K' = gamma^(L-1-s) K (zero past the ragged
       // end) split into hi | lo, and V split into hi (in place) | lo -- both re-laid from the TMA's
       // 128B swizzle (16-byte chunk j of row r at j ^ (r & 7)) to the MN-major tf32 layout
       // (32-byte granule g at g ^ (r & 3)), the only MN-major layout kind::tf32 reads.
-      for (int u = pt; u < (G::KB + 4) * kC; u += 96) {
+      if (!SO && TF32_TRUNC_INPLACE) {
+        // K' reads K (truncated in place by the prepA pass, possibly by another thread) + Klo
+        named_bar_sync(3, kPrep);
+      }
+      for (int u = pt; u < (G::KB + 4) * kC; u += kPrep) {
         const bool isv = u >= G::KB * kC;
         const int uu = isv ? u - G::KB * kC : u;
         const int r = uu & (kC - 1);
@@ -231,8 +254,8 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         float w = 1.f;
         if (!isv) {
           w = r < L ? pw[r < L ? L - 1 - r : 0] : 0.f;
-          if (!SO && TF32_TRUNC_INPLACE) {   // K was truncated in place: K = hi + lo exactly
-            const uint8_t* ls = smem + G::OFF_KLO + boff;
+          if (!SO && TF32_TRUNC_INPLACE) {   // K = hi + lo exactly
+            const uint8_t* ls = klo + boff;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float4 l = *reinterpret_cast<const float4*>(ls + ((j ^ (r & 7)) << 4));
@@ -240,14 +263,13 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             }
           }
         }
-        uint8_t* dh = isv ? (TF32_TRUNC_INPLACE ? vs + boff : nullptr) : smem + G::OFF_KPH + boff;
+        uint8_t* dh = isv ? vs + boff : smem + G::OFF_KPH + boff;
         uint8_t* dl = smem + (isv ? G::OFF_VLO : G::OFF_KPL) + boff;
-        if (isv && !TF32_TRUNC_INPLACE) {   // V keeps its raw bits as hi: only the relayout
-          dh = vs + boff;
-        }
+        const int flip = (r >> 2) & 1;   // rows r and r+4 store their halves in opposite order
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 v4 = x[j], h, l;
+        for (int jj = 0; jj < 8; ++jj) {
+          const int j = jj ^ flip;
+          float4 v4 = flip ? x[jj ^ 1] : x[jj], h, l;
           v4.x *= w; v4.y *= w; v4.z *= w; v4.w *= w;
           h.x = tf32_hi(v4.x); h.y = tf32_hi(v4.y); h.z = tf32_hi(v4.z); h.w = tf32_hi(v4.w);
           l.x = v4.x - h.x; l.y = v4.y - h.y; l.z = v4.z - h.z; l.w = v4.w - h.w;
@@ -258,8 +280,8 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       }
       fence_proxy_async_smem();
       if (dumping && c == 0) {   // raw smem of K, V (stage 0), K'hi, Vlo after prep: 4 x 4096 floats
-        named_bar_sync(3, 96);
-        for (int i = pt; i < 4096; i += 96) {
+        named_bar_sync(3, kPrep);
+        for (int i = pt; i < 4096; i += kPrep) {
           dump[20480 + i] = i < G::QK_BYTES / 4 ? reinterpret_cast<const float*>(ks)[i] : 0.f;
           dump[24576 + i] = reinterpret_cast<const float*>(vs)[i];
           dump[28672 + i] = i < G::QK_BYTES / 4 ? reinterpret_cast<const float*>(smem + G::OFF_KPH)[i] : 0.f;
@@ -280,7 +302,6 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const int jd = j0 + d;
     const bool dv_ok = jd < dv;
     const uint32_t lane_base = tbase + ((uint32_t)(sub * 32) << 16);
-    const bool leader = warp == 4 && lane == 0;
     float S[SC];
     auto publish = [&]() {
 #pragma unroll
@@ -321,6 +342,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       }
     }
     if (!SO && nch > 0) publish();
+    float* orow = SO ? nullptr : o + ((size_t)bh * N + lo) * dv + jd;
     for (int c = 0; c < nch; ++c) {
       const int L = min(kC, hi - lo - c * kC);
       mbar_wait(mma_s_bar, c & 1);
@@ -342,28 +364,19 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       mbar_wait(mma_o_bar, c & 1);                 // Oi, Ox done: S hi/lo may be replaced
       tc_fence_after();
       if (c != nch - 1) publish();
-      // ---- outputs: O[t][d] = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t], tokens g*16 .. g*16+15
-      float o[16], x[16];
-      tmem_ld16(lane_base + T_O + g * 16, o);
-      tmem_ld16(lane_base + T_OX + g * 16, x);
+      // ---- outputs: O[t][d] = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t], tokens g*16 .. g*16+15;
+      //      for each t the 32 lanes of a warp store 32 consecutive dv columns (128 B)
+      float ov[16], xv[16];
+      tmem_ld16(lane_base + T_O + g * 16, ov);
+      tmem_ld16(lane_base + T_OX + g * 16, xv);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(o_free);
-      if (leader) bulk_wait_read<0>();             // the previous chunk's store has read the tile
-      named_bar_sync(1, 256);
-      uint8_t* box = ot_smem + sub * 4096;         // d-block sub: [32 t][32 d] fp32, 128B swizzle
+      if (dv_ok) {
+        float* orc = orow + (size_t)(c * kC + g * 16) * dv;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int t = g * 16 + i;
-        const float val = fmaf(pw[t + 1], x[i], o[i]);
-        *reinterpret_cast<float*>(box + t * 128 + (((lane >> 2) ^ (t & 7)) << 4) + (lane & 3) * 4) = val;
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(2, 256);
-      if (leader) {
-#pragma unroll
-        for (int nb = 0; nb < 4; ++nb) tma_store_3d(&tm_o, ot_smem + nb * 4096, j0 + nb * 32, lo + c * kC, bh);
-        bulk_commit();
+        for (int i = 0; i < 16; ++i)
+          if (g * 16 + i < L) __stcs(orc + (size_t)i * dv, fmaf(pw[g * 16 + i + 1], xv[i], ov[i]));
       }
     }
     // end state: state-only launches write one local state per segment, full launches only the
@@ -374,7 +387,6 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       for (int i = 0; i < SC; ++i)
         if (col0 + i < dk) so[(size_t)(col0 + i) * dv] = S[i];
     }
-    if (leader) bulk_wait<0>();
   } else if (warp == 12) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -382,6 +394,18 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       for (int c = 0; c < nch; ++c) {
         const int s = c % STAGES;
         const int t0 = lo + c * kC;
+        // the ring is shallow (a stage is held until O_inter of its chunk): warm L2 with the chunk
+        // that will reuse this stage, so its load is an L2 hit when the stage frees
+        if (c + STAGES < nch) {
+          const int tp = t0 + STAGES * kC;
+#pragma unroll
+          for (int kb = 0; kb < G::KB; ++kb) {
+            if (!SO) tma_prefetch_l2_3d(&tm_q, kb * 32, tp, bh);
+            tma_prefetch_l2_3d(&tm_k, kb * 32, tp, bh);
+          }
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 32, tp, bh);
+        }
         mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
         uint8_t* st = smem + s * G::STAGE_BYTES;
         mbar_arrive_expect_tx(&full[s], bytes);
@@ -397,48 +421,56 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     }
   } else {
     // ------------------------------------------------------------ MMA issuer (whole warp)
-    constexpr uint32_t id_qk = idesc_tf32(128, kC, false, false);    // P^T = K Q^T
+    // per chunk: dS(c) -> Oi(c) -> MMA1(c+1) -> Ox(c); MMA1 runs ahead so the mask epilogue of
+    // c+1 overlaps the state publish that Ox(c) waits for
+    constexpr uint32_t id_qk = idesc_tf32(64, kC, false, false);     // P^T = K Q^T (M = 64)
     constexpr uint32_t id_vk = idesc_tf32(128, DKP, true, true);     // dS^T = V^T K'
     constexpr uint32_t id_vp = idesc_tf32(128, kC, true, true);      // Oi^T = V^T P^T
     constexpr uint32_t id_sq = idesc_tf32(128, kC, false, false);    // Ox^T = S^T(TMEM) Q^T
     const uint32_t base = smem_u32(smem);
-    const uint64_t dK0 = smem_desc_sw128(base, 16, 1024);             // K-major
+    const uint64_t dK0 = smem_desc_sw128(base, 16, 1024);             // K-major (TMA 128B swizzle)
     const uint64_t dM0 = smem_desc_sw128_b32(base, 4096, 512);        // MN-major tf32, 32-wide blocks
     constexpr uint64_t kStage = G::STAGE_BYTES >> 4, kQK = G::QK_BYTES >> 4;
-    const uint64_t klo_k = dK0 + (G::OFF_KLO >> 4), qlo_k = dK0 + (G::OFF_QLO >> 4);
+    const uint64_t klo_k0 = dK0 + (G::OFF_KLO >> 4);
     const uint64_t kph_m = dM0 + (G::OFF_KPH >> 4), kpl_m = dM0 + (G::OFF_KPL >> 4);
     const uint64_t vlo_m = dM0 + (G::OFF_VLO >> 4);
     const uint64_t ph_m = dM0 + (G::OFF_P >> 4), pl_m = ph_m + (4096 >> 4);
+    auto issue_mma1 = [&](int c) {
+      const int s = c % STAGES;
+      const uint64_t q_k = dK0 + s * kStage, k_k = q_k + kQK;
+      const uint64_t klo_k = klo_k0 + (c & 1) * 2 * kQK, qlo_k = klo_k + kQK;
+      mbar_wait(&full[s], (c / STAGES) & 1);
+      mbar_wait(&prepA[c & 1], (c >> 1) & 1);
+      tc_fence_after();
+      // P^T = Khi Qhi + Khi Qlo + Klo Qhi
+#pragma unroll
+      for (int kb = 0; kb < G::KB; ++kb)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t off = kb * 256 + kk * 2;
+          mma_tf32_ss_elect(tbase + T_P, k_k + off, q_k + off, id_qk, (kb | kk) != 0);
+          mma_tf32_ss_elect(tbase + T_P, k_k + off, qlo_k + off, id_qk, 1);
+          mma_tf32_ss_elect(tbase + T_P, klo_k + off, q_k + off, id_qk, 1);
+        }
+      mma_commit_elect(mma1_bar);
+    };
+    if (!SO && nch > 0) issue_mma1(0);
     for (int c = 0; c < nch; ++c) {
       const int s = c % STAGES;
-      const uint64_t q_k = dK0 + s * kStage, k_k = q_k + kQK;         // raw Q, K (hi), K-major
-      const uint64_t v_m = dM0 + s * kStage + 2 * kQK;                // raw V (hi), MN-major
-      mbar_wait(&full[s], (c / STAGES) & 1);
-      if (!SO) {
-        mbar_wait(prepA, c & 1);
-        tc_fence_after();
-        // P^T = Khi Qhi + Khi Qlo + Klo Qhi
-#pragma unroll
-        for (int kb = 0; kb < G::KB; ++kb)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t o = kb * 256 + kk * 2;
-            mma_tf32_ss_elect(tbase + T_P, k_k + o, q_k + o, id_qk, (kb | kk) != 0);
-            mma_tf32_ss_elect(tbase + T_P, k_k + o, qlo_k + o, id_qk, 1);
-            mma_tf32_ss_elect(tbase + T_P, klo_k + o, q_k + o, id_qk, 1);
-          }
-        mma_commit_elect(mma1_bar);
-      }
+      const uint64_t q_k = dK0 + s * kStage;                          // raw Q (hi), K-major
+      const uint64_t qlo_k = klo_k0 + (c & 1) * 2 * kQK + kQK;
+      const uint64_t v_m = dM0 + s * kStage + 2 * kQK;                // V (hi), MN-major
+      if (SO) mbar_wait(&full[s], (c / STAGES) & 1);
       mbar_wait(prepB, c & 1);
       if (c > 0) mbar_wait(ds_free, (c - 1) & 1);
       tc_fence_after();
       // dS^T = Vhi K'hi + Vhi K'lo + Vlo K'hi   (K step = 8 token rows = 1 KiB)
 #pragma unroll
       for (int ks = 0; ks < kC / 8; ++ks) {
-        const uint64_t o = ks * 64;
-        mma_tf32_ss_elect(tbase + T_DS, v_m + o, kph_m + o, id_vk, ks != 0);
-        mma_tf32_ss_elect(tbase + T_DS, v_m + o, kpl_m + o, id_vk, 1);
-        mma_tf32_ss_elect(tbase + T_DS, vlo_m + o, kph_m + o, id_vk, 1);
+        const uint64_t off = ks * 64;
+        mma_tf32_ss_elect(tbase + T_DS, v_m + off, kph_m + off, id_vk, ks != 0);
+        mma_tf32_ss_elect(tbase + T_DS, v_m + off, kpl_m + off, id_vk, 1);
+        mma_tf32_ss_elect(tbase + T_DS, vlo_m + off, kph_m + off, id_vk, 1);
       }
       mma_commit_elect(mma_s_bar);
       if (!SO) {
@@ -448,13 +480,14 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         // Oi^T = Vhi Phi + Vhi Plo + Vlo Phi
 #pragma unroll
         for (int ks = 0; ks < kC / 8; ++ks) {
-          const uint64_t o = ks * 64;
-          mma_tf32_ss_elect(tbase + T_O, v_m + o, ph_m + o, id_vp, ks != 0);
-          mma_tf32_ss_elect(tbase + T_O, v_m + o, pl_m + o, id_vp, 1);
-          mma_tf32_ss_elect(tbase + T_O, vlo_m + o, ph_m + o, id_vp, 1);
+          const uint64_t off = ks * 64;
+          mma_tf32_ss_elect(tbase + T_O, v_m + off, ph_m + off, id_vp, ks != 0);
+          mma_tf32_ss_elect(tbase + T_O, v_m + off, pl_m + off, id_vp, 1);
+          mma_tf32_ss_elect(tbase + T_O, vlo_m + off, ph_m + off, id_vp, 1);
         }
         mma_commit_elect(p_free);
         mma_commit_elect(derB_free);
+        if (c + 1 < nch) issue_mma1(c + 1);
         mbar_wait(st_full, c & 1);
         tc_fence_after();
         // Ox^T = Shi Qhi + Shi Qlo + Slo Qhi   (A from TMEM: 8 columns per K step)
@@ -462,14 +495,14 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         for (int kb = 0; kb < G::KB; ++kb)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t o = kb * 256 + kk * 2;
+            const uint64_t off = kb * 256 + kk * 2;
             const uint32_t col = (kb * 4 + kk) * 8;
-            mma_tf32_ts_elect(tbase + T_OX, tbase + T_SHI + col, q_k + o, id_sq, (kb | kk) != 0);
-            mma_tf32_ts_elect(tbase + T_OX, tbase + T_SHI + col, qlo_k + o, id_sq, 1);
-            mma_tf32_ts_elect(tbase + T_OX, tbase + T_SLO + col, q_k + o, id_sq, 1);
+            mma_tf32_ts_elect(tbase + T_OX, tbase + T_SHI + col, q_k + off, id_sq, (kb | kk) != 0);
+            mma_tf32_ts_elect(tbase + T_OX, tbase + T_SHI + col, qlo_k + off, id_sq, 1);
+            mma_tf32_ts_elect(tbase + T_OX, tbase + T_SLO + col, q_k + off, id_sq, 1);
           }
         mma_commit_elect(mma_o_bar);
-        mma_commit_elect(derA_free);
+        mma_commit_elect(&derA_free[c & 1]);
       } else {
         mma_commit_elect(derB_free);
       }
@@ -505,18 +538,16 @@ cudaError_t launch_v4(const void* q, const void* k, const void* v, void* o, cons
   using G = v4::Cfg<DKP, STAGES>;
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
   const int64_t BH = s.B * s.H;
-  CUtensorMap mq, mk, mv, mo;
+  CUtensorMap mq, mk, mv;
   if (!make_map_f32(&mk, k, s.dk, s.N, BH) || !make_map_f32(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
   mq = mk;
-  mo = mv;
-  if (!SO && (!make_map_f32(&mq, q, s.dk, s.N, BH) || !make_map_f32(&mo, o, s.dv, s.N, BH)))
-    return cudaErrorInvalidValue;
+  if (!SO && !make_map_f32(&mq, q, s.dk, s.N, BH)) return cudaErrorInvalidValue;
   auto kern = v4::prefill_tf32_kernel<DKP, STAGES, SO>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
   const dim3 grid((unsigned)((s.dv + v4::kDVT - 1) / v4::kDVT), (unsigned)BH, (unsigned)nz);
-  err = launch_pdl(kern, grid, dim3(v4::kThreads), G::SMEM, stream, mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H,
-                   (int)s.N, (int)s.dk, (int)s.dv, sa, g_tf32_dump);
+  err = launch_pdl(kern, grid, dim3(v4::kThreads), G::SMEM, stream, mq, mk, mv, static_cast<float*>(o), log2g,
+                   s_in, s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, sa, g_tf32_dump);
   if (err != cudaSuccess) return err;
   count_launch();
   return cudaGetLastError();
