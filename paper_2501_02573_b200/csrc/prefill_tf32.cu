@@ -63,42 +63,49 @@ constexpr uint32_t T_P = 0, T_OX = 32, T_O = 64, T_DS = 128, T_SHI = 256, T_SLO 
 // Shared memory (1 KiB aligned).  Q/K/V tiles are TMA boxes of [32 rows][32 fp32] (4 KiB, 128-byte
 // swizzle), column blocks 4 KiB apart.  MMA1 reads K as a 128-row A operand (rows 32..127 are
 // don't-care), i.e. 12 KiB past the last K box: K is followed by V in the stage, Klo by Qlo.
-template <int DKP, int STAGES>
+// Two TMA rings: Q (QST stages, held until O_inter of its chunk) and K|V (KVST stages, released
+// after O_intra), so the next K/V loads start a whole MMA1 + O_inter earlier than with one ring.
+template <int DKP, int QST, int KVST>
 struct Cfg {
   static constexpr int KB = DKP / 32;
   static constexpr int QK_BYTES = kC * DKP * 4;
   static constexpr int V_BYTES = kC * kDVT * 4;
-  static constexpr int STAGE_BYTES = 2 * QK_BYTES + V_BYTES;     // Q | K | V
-  static constexpr int OFF_KLO = STAGES * STAGE_BYTES;             // [2] x (Klo | Qlo), K-major
-  static constexpr int OFF_KPH = OFF_KLO + 4 * QK_BYTES;           // K'hi | K'lo | Vlo, MN-major
+  static constexpr int KV_BYTES = QK_BYTES + V_BYTES;              // K | V
+  static constexpr int OFF_KV = QST * QK_BYTES;
+  static constexpr int OFF_KLO = OFF_KV + KVST * KV_BYTES;         // Klo | Qlo[2], K-major
+  static constexpr int OFF_QLO = OFF_KLO + QK_BYTES;
+  static constexpr int OFF_KPH = OFF_QLO + 2 * QK_BYTES;           // K'hi | K'lo | Vlo, MN-major
   static constexpr int OFF_KPL = OFF_KPH + QK_BYTES;
   static constexpr int OFF_VLO = OFF_KPL + QK_BYTES;
   static constexpr int OFF_P = OFF_VLO + V_BYTES;                  // P^T hi | lo [32 s][32 t]
   static constexpr int OFF_POW = OFF_P + 2 * 4096;                 // gamma^n, n = 0..32
   static constexpr int OFF_BAR = OFF_POW + 64 * 4;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  // the 64-row A operand of MMA1 reads 4 KiB past the last K box (K then V in the stage, Klo then Qlo)
-  static_assert((KB + 1) * 4096 <= QK_BYTES + V_BYTES && (KB + 1) * 4096 <= 2 * QK_BYTES, "A overread");
+  static constexpr int SMEM = OFF_BAR + 512 + 1024;
+  // the 64-row A operand of MMA1 reads 4 KiB past the last K box (K then V in a K|V stage, Klo then Qlo)
+  static_assert((KB + 1) * 4096 <= KV_BYTES && (KB + 1) * 4096 <= 3 * QK_BYTES, "A overread");
 };
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-template <int DKP, int STAGES, bool SO>
+template <int DKP, int QST, int KVST, bool SO>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, float* __restrict__ o,
                     const float* __restrict__ log2g, const float* __restrict__ s_in, float* __restrict__ s_out,
                     int H, int N, int dk, int dv, const SegArgs sa, float* __restrict__ dump) {
-  using G = Cfg<DKP, STAGES>;
+  using G = Cfg<DKP, QST, KVST>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // aligned by pointer arithmetic (not via an integer cast) so ptxas keeps the shared address
   // space: LDS/STS instead of generic loads/stores
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
-  uint64_t* empty = full + STAGES;
-  uint64_t* prepA = empty + STAGES;      // [2] Klo, Qlo of buffer b written (128 arrivals)
-  uint64_t* derA_free = prepA + 2;       // [2] MMA1 + Ox done with buffer b (commit)
-  uint64_t* prepB = derA_free + 2;       // K'hi, K'lo, Vlo written (128)
+  uint64_t* full_q = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* empty_q = full_q + QST;
+  uint64_t* full_kv = empty_q + QST;
+  uint64_t* empty_kv = full_kv + KVST;
+  uint64_t* prepA = empty_kv + KVST;     // [2] Klo, Qlo[b] written (128 arrivals)
+  uint64_t* derA_free = prepA + 2;       // [2] Ox done with Qlo[b] (commit)
+  uint64_t* klo_free = derA_free + 2;    // MMA1 done with Klo (commit)
+  uint64_t* prepB = klo_free + 1;        // K'hi, K'lo, Vlo written (128)
   uint64_t* derB_free = prepB + 1;       // dS + Oi done with K'/Vlo (commit)
   uint64_t* mma1_bar = derB_free + 1;    // P^T in TMEM (commit)
   uint64_t* mask_bar = mma1_bar + 1;     // P^T hi/lo in smem, TMEM copy read (64)
@@ -121,10 +128,15 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   const size_t per_state = (size_t)gridDim.y * dk * dv;
 
   if (warp == 12 && lane == 0) {
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+    for (int i = 0; i < QST; ++i) {
+      mbar_init(&full_q[i], 1);
+      mbar_init(&empty_q[i], 1);
     }
+    for (int i = 0; i < KVST; ++i) {
+      mbar_init(&full_kv[i], 1);
+      mbar_init(&empty_kv[i], 1);
+    }
+    mbar_init(klo_free, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&prepA[b], kPrep);
       mbar_init(&derA_free[b], 1);
@@ -206,18 +218,19 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     // ------------------------------------------------------------ operand prep (128 threads)
     const int pt = warp < 4 ? (int)threadIdx.x - 64 : (int)threadIdx.x - 384;
     for (int c = 0; c < nch; ++c) {
-      const int s = c % STAGES;
+      const int sq = c % QST, skv = c % KVST;
       const int b = c & 1;
       const int L = min(kC, hi - lo - c * kC);
-      uint8_t* st = smem + s * G::STAGE_BYTES;
-      uint8_t* qs = st;
-      uint8_t* ks = st + G::QK_BYTES;
-      uint8_t* vs = st + 2 * G::QK_BYTES;
-      uint8_t* klo = smem + G::OFF_KLO + b * 2 * G::QK_BYTES;
-      uint8_t* qlo = klo + G::QK_BYTES;
-      mbar_wait(&full[s], (c / STAGES) & 1);
+      uint8_t* qs = smem + sq * G::QK_BYTES;
+      uint8_t* ks = smem + G::OFF_KV + skv * G::KV_BYTES;
+      uint8_t* vs = ks + G::QK_BYTES;
+      uint8_t* klo = smem + G::OFF_KLO;
+      uint8_t* qlo = smem + G::OFF_QLO + b * G::QK_BYTES;
+      mbar_wait(&full_kv[skv], (c / KVST) & 1);
       if (!SO) {
+        mbar_wait(&full_q[sq], (c / QST) & 1);
         if (c >= 2) mbar_wait(&derA_free[b], ((c >> 1) - 1) & 1);
+        if (c >= 1) mbar_wait(klo_free, (c - 1) & 1);
         // Klo, Qlo (and, with TF32_TRUNC_INPLACE, the hi parts truncated in place)
         for (int i = pt; i < 2 * G::QK_BYTES / 16; i += kPrep) {
           const bool isk = i < G::QK_BYTES / 16;
@@ -390,14 +403,12 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   } else if (warp == 12) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      const uint32_t bytes = (SO ? 0 : G::QK_BYTES) + G::QK_BYTES + G::V_BYTES;
       for (int c = 0; c < nch; ++c) {
-        const int s = c % STAGES;
+        const int sq = c % QST, skv = c % KVST;
         const int t0 = lo + c * kC;
-        // the ring is shallow (a stage is held until O_inter of its chunk): warm L2 with the chunk
-        // that will reuse this stage, so its load is an L2 hit when the stage frees
-        if (c + STAGES < nch) {
-          const int tp = t0 + STAGES * kC;
+        // warm L2 with the chunk that will reuse this K|V stage, so its load is an L2 hit
+        if (c + KVST < nch) {
+          const int tp = t0 + KVST * kC;
 #pragma unroll
           for (int kb = 0; kb < G::KB; ++kb) {
             if (!SO) tma_prefetch_l2_3d(&tm_q, kb * 32, tp, bh);
@@ -406,17 +417,21 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 #pragma unroll
           for (int nb = 0; nb < 4; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 32, tp, bh);
         }
-        mbar_wait(&empty[s], ((c / STAGES) & 1) ^ 1);
-        uint8_t* st = smem + s * G::STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[s], bytes);
+        if (!SO) {
+          mbar_wait(&empty_q[sq], ((c / QST) & 1) ^ 1);
+          uint8_t* qd = smem + sq * G::QK_BYTES;
+          mbar_arrive_expect_tx(&full_q[sq], G::QK_BYTES);
 #pragma unroll
-        for (int kb = 0; kb < G::KB; ++kb) {
-          if (!SO) tma_load_3d(st + kb * 4096, &tm_q, &full[s], kb * 32, t0, bh);
-          tma_load_3d(st + G::QK_BYTES + kb * 4096, &tm_k, &full[s], kb * 32, t0, bh);
+          for (int kb = 0; kb < G::KB; ++kb) tma_load_3d(qd + kb * 4096, &tm_q, &full_q[sq], kb * 32, t0, bh);
         }
+        mbar_wait(&empty_kv[skv], ((c / KVST) & 1) ^ 1);
+        uint8_t* kd = smem + G::OFF_KV + skv * G::KV_BYTES;
+        mbar_arrive_expect_tx(&full_kv[skv], G::KV_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb) tma_load_3d(kd + kb * 4096, &tm_k, &full_kv[skv], kb * 32, t0, bh);
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb)
-          tma_load_3d(st + 2 * G::QK_BYTES + nb * 4096, &tm_v, &full[s], j0 + nb * 32, t0, bh);
+          tma_load_3d(kd + G::QK_BYTES + nb * 4096, &tm_v, &full_kv[skv], j0 + nb * 32, t0, bh);
       }
     }
   } else {
@@ -430,16 +445,17 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const uint32_t base = smem_u32(smem);
     const uint64_t dK0 = smem_desc_sw128(base, 16, 1024);             // K-major (TMA 128B swizzle)
     const uint64_t dM0 = smem_desc_sw128_b32(base, 4096, 512);        // MN-major tf32, 32-wide blocks
-    constexpr uint64_t kStage = G::STAGE_BYTES >> 4, kQK = G::QK_BYTES >> 4;
-    const uint64_t klo_k0 = dK0 + (G::OFF_KLO >> 4);
+    constexpr uint64_t kQK = G::QK_BYTES >> 4, kKV = G::KV_BYTES >> 4;
+    const uint64_t klo_k = dK0 + (G::OFF_KLO >> 4), qlo_k0 = dK0 + (G::OFF_QLO >> 4);
+    const uint64_t kv_k0 = dK0 + (G::OFF_KV >> 4), kv_m0 = dM0 + (G::OFF_KV >> 4);
     const uint64_t kph_m = dM0 + (G::OFF_KPH >> 4), kpl_m = dM0 + (G::OFF_KPL >> 4);
     const uint64_t vlo_m = dM0 + (G::OFF_VLO >> 4);
     const uint64_t ph_m = dM0 + (G::OFF_P >> 4), pl_m = ph_m + (4096 >> 4);
     auto issue_mma1 = [&](int c) {
-      const int s = c % STAGES;
-      const uint64_t q_k = dK0 + s * kStage, k_k = q_k + kQK;
-      const uint64_t klo_k = klo_k0 + (c & 1) * 2 * kQK, qlo_k = klo_k + kQK;
-      mbar_wait(&full[s], (c / STAGES) & 1);
+      const uint64_t q_k = dK0 + (c % QST) * kQK, k_k = kv_k0 + (c % KVST) * kKV;
+      const uint64_t qlo_k = qlo_k0 + (c & 1) * kQK;
+      mbar_wait(&full_q[c % QST], (c / QST) & 1);
+      mbar_wait(&full_kv[c % KVST], (c / KVST) & 1);
       mbar_wait(&prepA[c & 1], (c >> 1) & 1);
       tc_fence_after();
       // P^T = Khi Qhi + Khi Qlo + Klo Qhi
@@ -453,14 +469,15 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           mma_tf32_ss_elect(tbase + T_P, klo_k + off, q_k + off, id_qk, 1);
         }
       mma_commit_elect(mma1_bar);
+      mma_commit_elect(klo_free);
     };
     if (!SO && nch > 0) issue_mma1(0);
     for (int c = 0; c < nch; ++c) {
-      const int s = c % STAGES;
-      const uint64_t q_k = dK0 + s * kStage;                          // raw Q (hi), K-major
-      const uint64_t qlo_k = klo_k0 + (c & 1) * 2 * kQK + kQK;
-      const uint64_t v_m = dM0 + s * kStage + 2 * kQK;                // V (hi), MN-major
-      if (SO) mbar_wait(&full[s], (c / STAGES) & 1);
+      const int sq = c % QST, skv = c % KVST;
+      const uint64_t q_k = dK0 + sq * kQK;                            // raw Q (hi), K-major
+      const uint64_t qlo_k = qlo_k0 + (c & 1) * kQK;
+      const uint64_t v_m = kv_m0 + skv * kKV + kQK;                   // V (hi), MN-major
+      mbar_wait(&full_kv[skv], (c / KVST) & 1);
       mbar_wait(prepB, c & 1);
       if (c > 0) mbar_wait(ds_free, (c - 1) & 1);
       tc_fence_after();
@@ -487,6 +504,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         mma_commit_elect(p_free);
         mma_commit_elect(derB_free);
+        mma_commit_elect(&empty_kv[skv]);            // K (MMA1, K') and V (dS, Oi) consumed
         if (c + 1 < nch) issue_mma1(c + 1);
         mbar_wait(st_full, c & 1);
         tc_fence_after();
@@ -503,10 +521,11 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           }
         mma_commit_elect(mma_o_bar);
         mma_commit_elect(&derA_free[c & 1]);
+        mma_commit_elect(&empty_q[sq]);
       } else {
         mma_commit_elect(derB_free);
+        mma_commit_elect(&empty_kv[skv]);
       }
-      mma_commit_elect(&empty[s]);
     }
   }
 
@@ -532,17 +551,17 @@ bool make_map_f32(CUtensorMap* map, const void* base, int64_t D, int64_t N, int6
   return r == CUDA_SUCCESS;
 }
 
-template <int DKP, int STAGES, bool SO>
+template <int DKP, int QST, int KVST, bool SO>
 cudaError_t launch_v4(const void* q, const void* k, const void* v, void* o, const float* log2g, const float* s_in,
                       float* s_out, const ShapeArgs& s, const SegArgs& sa, int nz, cudaStream_t stream) {
-  using G = v4::Cfg<DKP, STAGES>;
+  using G = v4::Cfg<DKP, QST, KVST>;
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
   const int64_t BH = s.B * s.H;
   CUtensorMap mq, mk, mv;
   if (!make_map_f32(&mk, k, s.dk, s.N, BH) || !make_map_f32(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
   mq = mk;
   if (!SO && !make_map_f32(&mq, q, s.dk, s.N, BH)) return cudaErrorInvalidValue;
-  auto kern = v4::prefill_tf32_kernel<DKP, STAGES, SO>;
+  auto kern = v4::prefill_tf32_kernel<DKP, QST, KVST, SO>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
   const dim3 grid((unsigned)((s.dv + v4::kDVT - 1) / v4::kDVT), (unsigned)BH, (unsigned)nz);
@@ -581,13 +600,13 @@ cudaError_t launch_prefill_tf32(const void* q, const void* k, const void* v, voi
     if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return cudaErrorNotSupported;
   if (!tf32_supported(s, LINATTN_F32)) return cudaErrorNotSupported;
   if (s.dk <= 32)
-    return state_only ? launch_v4<32, 6, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
-                      : launch_v4<32, 6, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
+    return state_only ? launch_v4<32, 4, 5, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
+                      : launch_v4<32, 4, 5, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
   if (s.dk <= 64)
-    return state_only ? launch_v4<64, 4, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
-                      : launch_v4<64, 4, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
-  return state_only ? launch_v4<128, 2, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
-                    : launch_v4<128, 2, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
+    return state_only ? launch_v4<64, 4, 4, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
+                      : launch_v4<64, 4, 4, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
+  return state_only ? launch_v4<128, 3, 2, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
+                    : launch_v4<128, 3, 2, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
 }
 
 }  // namespace linattn
