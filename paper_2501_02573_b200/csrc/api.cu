@@ -273,6 +273,21 @@ int linattn_prefill(const void* q, const void* k, const void* v, void* o, const 
     }
     cudaGetLastError();
   }
+  // 3xTF32 kernel (tensor-pipe bound, one CTA per SM): balanced whenever the units leave a
+  // partly filled last wave
+  if (fam == FAM_TF32 && balance_env != 0) {
+    const int tctas = balance_env == 2 ? ctas : tf32_balance_ctas(s, ctas);   // 2: force (dev A/B)
+    if (tctas > 0) {
+      void* ws = nullptr;
+      cudaMemPool_t pool = work_pool();
+      if (pool && cudaMallocFromPoolAsync(&ws, tf32_balance_workspace_bytes(s, tctas), pool, st) == cudaSuccess) {
+        cudaError_t e = launch_prefill_tf32_balanced(q, k, v, o, log2g, s_in, s_out, s, tctas, ws, st);
+        cudaFreeAsync(ws, st);
+        if (e != cudaErrorNotSupported) return cuda_status(e, "prefill_tf32 (balanced)");
+      }
+      cudaGetLastError();
+    }
+  }
   // FFMA kernel (compute-bound, two or more CTAs per SM): the same schedule over the resident
   // slots whenever the units are not a whole number of waves
   if (fam == FAM_SIMT && balance_env != 0) {

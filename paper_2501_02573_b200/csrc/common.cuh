@@ -186,6 +186,14 @@ cudaError_t launch_prefill_tf32(const void* q, const void* k, const void* v, voi
                                 const float* s_in, float* s_out, const ShapeArgs& s, bool state_only,
                                 const SegArgs& sa, int nz, cudaStream_t stream);
 
+// Balanced persistent 3xTF32 prefill (one CTA per SM over equal chunk ranges with head -> tail
+// state hand-off): grid for this shape or 0 (keep the plain grid); workspace bytes; launcher.
+int tf32_balance_ctas(const ShapeArgs& s, int sms);
+size_t tf32_balance_workspace_bytes(const ShapeArgs& s, int ctas);
+cudaError_t launch_prefill_tf32_balanced(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                                         const float* s_in, float* s_out, const ShapeArgs& s, int ctas, void* ws,
+                                         cudaStream_t stream);
+
 // Returns cudaErrorNotSupported when the shape is outside the TC kernel's envelope.
 cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void* o,
                               const float* log2g, const float* s_in, float* s_out,

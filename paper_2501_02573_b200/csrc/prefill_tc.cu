@@ -519,6 +519,9 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       // the tensor pipe sees one flat chunk stream across the work list (c counts every chunk)
       int nchunks = 0;
       for (int it = 0; it < nitems; ++it) nchunks += item_chunks(item(it));
+      // lane-0 broadcast: a provably warp-uniform chunk count keeps the descriptors in uniform
+      // registers (otherwise ptxas wraps every tcgen05.mma of the balanced build in an R2UR loop)
+      nchunks = __shfl_sync(0xffffffffu, nchunks, 0);
       if (!state_only && nchunks > 0) issue_mma1(0);
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % STAGES;
@@ -1157,6 +1160,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       const WorkItem w = item(it);
       nchunks += w.hi > w.lo ? (w.hi - w.lo + kC - 1) / kC : 0;
     }
+    nchunks = __shfl_sync(0xffffffffu, nchunks, 0);   // warp-uniform: descriptors stay in uniform registers
     if (!state_only && nchunks > 0) issue_mma1(0);
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % STAGES;

@@ -37,6 +37,21 @@
 #include "common.cuh"
 #include "sm100.cuh"
 
+#ifndef TF32_BAL_ONEITEM
+#define TF32_BAL_ONEITEM 0     // dev bisect: balance_item items, but a compile-time item count of 1
+#endif
+#ifndef TF32_BAL_PLAINITEM
+#define TF32_BAL_PLAINITEM 0   // dev bisect: BAL instantiation with the plain one-unit-per-CTA items
+#endif
+#ifndef TF32_BAL_REGS
+#define TF32_BAL_REGS 0
+#endif
+#ifndef TF32_BAL_PDL
+#define TF32_BAL_PDL 0
+#endif
+#ifndef TF32_L2_PREFETCH
+#define TF32_L2_PREFETCH 1     // warm L2 with the chunk that will reuse a K|V stage
+#endif
 #ifndef TF32_TRUNC_INPLACE
 #define TF32_TRUNC_INPLACE 0   // 1: also clear the low mantissa bits of the TMA-loaded hi operands (the
                                // MMA ignores them: bit-identical results measured on B200, so off)
@@ -79,7 +94,7 @@ struct Cfg {
   static constexpr int OFF_VLO = OFF_KPL + QK_BYTES;
   static constexpr int OFF_P = OFF_VLO + V_BYTES;                  // P^T hi | lo [32 s][32 t]
   static constexpr int OFF_POW = OFF_P + 2 * 4096;                 // gamma^n, n = 0..32
-  static constexpr int OFF_BAR = OFF_POW + 64 * 4;
+  static constexpr int OFF_BAR = OFF_POW + 3 * 64 * 4;            // (three per-role tables)
   static constexpr int SMEM = OFF_BAR + 512 + 1024;
   // the 64-row A operand of MMA1 reads 4 KiB past the last K box (K then V in a K|V stage, Klo then Qlo)
   static_assert((KB + 1) * 4096 <= KV_BYTES && (KB + 1) * 4096 <= 3 * QK_BYTES, "A overread");
@@ -87,12 +102,12 @@ struct Cfg {
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-template <int DKP, int QST, int KVST, bool SO>
+template <int DKP, int QST, int KVST, bool SO, bool BAL>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, float* __restrict__ o,
                     const float* __restrict__ log2g, const float* __restrict__ s_in, float* __restrict__ s_out,
-                    int H, int N, int dk, int dv, const SegArgs sa, float* __restrict__ dump) {
+                    int H, int N, int dk, int dv, const SegArgs sa, const Balance bal, float* __restrict__ dump) {
   using G = Cfg<DKP, QST, KVST>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // aligned by pointer arithmetic (not via an integer cast) so ptxas keeps the shared address
@@ -116,18 +131,29 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   uint64_t* mma_o_bar = st_full + 1;     // Oi + Ox done (commit)
   uint64_t* o_free = mma_o_bar + 1;      // O / Ox drained (256)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
-  float* pw = reinterpret_cast<float*>(smem + G::OFF_POW);
+  // work-list header {ticket, items, range start, range end}, re-read at item boundaries
+  int* wl = reinterpret_cast<int*>(tmem_slot + 2);
+  // per-role gamma^n tables (n = 0..32): mask | prep | state, each rewritten by its own role at
+  // an item boundary (balanced ranges span heads)
+  float* pw_mask = reinterpret_cast<float*>(smem + G::OFF_POW);
+  float* pw_prep = pw_mask + 64;
+  float* pw_st = pw_mask + 128;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
-  const int bh = blockIdx.y;
-  const int j0 = blockIdx.x * kDVT;
-  int lo, hi;
-  seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, lo, hi);
-  const int nch = hi > lo ? (hi - lo + kC - 1) / kC : 0;
   const size_t per_state = (size_t)gridDim.y * dk * dv;
 
   if (warp == 12 && lane == 0) {
+    if constexpr (BAL) {   // tickets in start order: the range before ours is already running
+      const int t = (int)atomicAdd(bal.flags + gridDim.x, 1u);
+      long long r0 = 0, r1 = 0;
+      wl[1] = balance_items(bal, t, r0, r1);
+      wl[0] = t;
+      reinterpret_cast<long long*>(wl)[1] = r0;
+      reinterpret_cast<long long*>(wl)[2] = r1;
+    } else {
+      wl[1] = 1;
+    }
     for (int i = 0; i < QST; ++i) {
       mbar_init(&full_q[i], 1);
       mbar_init(&empty_q[i], 1);
@@ -159,14 +185,41 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   if (warp == 13) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
-  pdl_wait();   // the prologue above overlapped the previous kernel's tail
-  const float lg = log2g[bh % H];
-  if (threadIdx.x <= kC) pw[threadIdx.x] = gpow(lg, (float)threadIdx.x);
-  __syncthreads();
+  if constexpr (!BAL || TF32_BAL_PDL) pdl_wait();   // the prologue above overlapped the previous kernel's tail
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const bool dumping = dump != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
-  if (dumping && threadIdx.x <= kC) dump[threadIdx.x] = pw[threadIdx.x];
+  const int nitems = BAL && !TF32_BAL_PLAINITEM && !TF32_BAL_ONEITEM ? wl[1] : 1;
+#if TF32_BAL_REGS
+  const int wl_t = wl[0];
+  const long long wl_r0 = reinterpret_cast<const long long*>(wl)[1], wl_r1 = reinterpret_cast<const long long*>(wl)[2];
+#endif
+  auto item = [&](int k) {
+    if constexpr (BAL && !TF32_BAL_PLAINITEM) {
+#if TF32_BAL_REGS
+      return balance_item(bal, N, wl_t, k, wl_r0, wl_r1);
+#else
+      const volatile int* v = wl;
+      const volatile long long* r = reinterpret_cast<const volatile long long*>(wl);
+      return balance_item(bal, N, v[0], k, r[1], r[2]);
+#endif
+    }
+    WorkItem w;
+    w.bh = TF32_BAL_PLAINITEM && BAL ? (TF32_BAL_PLAINITEM == 2 ? (blockIdx.x * 37) % gridDim.x
+                                        : TF32_BAL_PLAINITEM == 3 ? wl[0] : blockIdx.x) : blockIdx.y;
+    w.j0 = TF32_BAL_PLAINITEM && BAL ? 0 : blockIdx.x * kDVT;
+    seg_bounds(sa.seg_len, sa.sub, sa.m, blockIdx.z, N, w.lo, w.hi);
+    w.in_slot = w.out_slot = -1;
+    return w;
+  };
+  auto item_chunks = [](const WorkItem& w) { return w.hi > w.lo ? (w.hi - w.lo + kC - 1) / kC : 0; };
+  // rewrite a role's gamma table for the item's head (every role thread done with the old one first)
+  auto load_table = [&](float* tab, const WorkItem& w, int it, int rank, int nthr, int bar_id) {
+    if (it > 0) named_bar_sync(bar_id, nthr);
+    const float lgi = log2g[w.bh % H];
+    for (int n = rank; n <= kC; n += nthr) tab[n] = gpow(lgi, (float)n);
+    named_bar_sync(bar_id, nthr);
+  };
+  const bool dumping = !BAL && dump != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
 
   if (warp < 2) {
     // ------------------------------------------------------------ P^T mask + hi/lo split
@@ -176,61 +229,72 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       const bool live = lane < 16;
       uint8_t* ph = smem + G::OFF_P;
       uint8_t* pl = ph + 4096;
-      for (int c = 0; c < nch; ++c) {
-        mbar_wait(mma1_bar, c & 1);
-        tc_fence_after();
-        float p[32];
-        tmem_ld32(tbase + ((32 * warp) << 16) + T_P, p);
-        tmem_wait_ld();
-        if (dumping && c == 0 && live)
-          for (int t = 0; t < 32; ++t) dump[64 + srow * 32 + t] = p[t];
-        if (c > 0) mbar_wait(p_free, (c - 1) & 1);    // Oi(c-1) has read the previous P^T
-        if (live) {
-          float hv[32], lv[32];
+      int gc = 0;
+      for (int it = 0; it < nitems; ++it) {
+        const WorkItem w = item(it);
+        load_table(pw_mask, w, it, (int)threadIdx.x, 64, 4);
+        const int nch = item_chunks(w);
+        for (int c = 0; c < nch; ++c, ++gc) {
+          mbar_wait(mma1_bar, gc & 1);
+          tc_fence_after();
+          float p[32];
+          tmem_ld32(tbase + ((32 * warp) << 16) + T_P, p);
+          tmem_wait_ld();
+          if (dumping && gc == 0 && live)
+            for (int t = 0; t < 32; ++t) dump[64 + srow * 32 + t] = p[t];
+          if (gc > 0) mbar_wait(p_free, (gc - 1) & 1);    // Oi(gc-1) has read the previous P^T
+          if (live) {
+            float hv[32], lv[32];
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const float x = t >= srow ? p[t] * pw[t >= srow ? t - srow : 0] : 0.f;
-            hv[t] = tf32_hi(x);
-            lv[t] = x - hv[t];
-          }
-          // MN-major tf32 layout: 16-byte piece j of row s at granule (j/2) ^ (s & 3), half j & 1.
-          // Rows s and s+4 share granule positions, so they store the two halves in opposite
-          // order (jj ^ flip) and a quarter-warp never hits one bank twice.
-          const int flip = (srow >> 2) & 1;
+            for (int t = 0; t < 32; ++t) {
+              const float x = t >= srow ? p[t] * pw_mask[t >= srow ? t - srow : 0] : 0.f;
+              hv[t] = tf32_hi(x);
+              lv[t] = x - hv[t];
+            }
+            // MN-major tf32 layout: 16-byte piece j of row s at granule (j/2) ^ (s & 3), half j & 1.
+            // Rows s and s+4 share granule positions, so they store the two halves in opposite
+            // order (jj ^ flip) and a quarter-warp never hits one bank twice.
+            const int flip = (srow >> 2) & 1;
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const int j = jj ^ flip;
-            const int off = srow * 128 + (((((j >> 1) ^ (srow & 3)) << 1) | (j & 1)) << 4);
-            const float4 h4 = flip ? make_float4(hv[4 * (jj ^ 1)], hv[4 * (jj ^ 1) + 1], hv[4 * (jj ^ 1) + 2], hv[4 * (jj ^ 1) + 3])
-                                   : make_float4(hv[4 * jj], hv[4 * jj + 1], hv[4 * jj + 2], hv[4 * jj + 3]);
-            const float4 l4 = flip ? make_float4(lv[4 * (jj ^ 1)], lv[4 * (jj ^ 1) + 1], lv[4 * (jj ^ 1) + 2], lv[4 * (jj ^ 1) + 3])
-                                   : make_float4(lv[4 * jj], lv[4 * jj + 1], lv[4 * jj + 2], lv[4 * jj + 3]);
-            *reinterpret_cast<float4*>(ph + off) = h4;
-            *reinterpret_cast<float4*>(pl + off) = l4;
+            for (int jj = 0; jj < 8; ++jj) {
+              const int j = jj ^ flip;
+              const int off = srow * 128 + (((((j >> 1) ^ (srow & 3)) << 1) | (j & 1)) << 4);
+              const float4 h4 = flip ? make_float4(hv[4 * (jj ^ 1)], hv[4 * (jj ^ 1) + 1], hv[4 * (jj ^ 1) + 2], hv[4 * (jj ^ 1) + 3])
+                                     : make_float4(hv[4 * jj], hv[4 * jj + 1], hv[4 * jj + 2], hv[4 * jj + 3]);
+              const float4 l4 = flip ? make_float4(lv[4 * (jj ^ 1)], lv[4 * (jj ^ 1) + 1], lv[4 * (jj ^ 1) + 2], lv[4 * (jj ^ 1) + 3])
+                                     : make_float4(lv[4 * jj], lv[4 * jj + 1], lv[4 * jj + 2], lv[4 * jj + 3]);
+              *reinterpret_cast<float4*>(ph + off) = h4;
+              *reinterpret_cast<float4*>(pl + off) = l4;
+            }
           }
+          fence_proxy_async_smem();
+          tc_fence_before();
+          mbar_arrive(mask_bar);
         }
-        fence_proxy_async_smem();
-        tc_fence_before();
-        mbar_arrive(mask_bar);
       }
     }
   } else if (warp < 4 || warp >= 14) {
     // ------------------------------------------------------------ operand prep (128 threads)
     const int pt = warp < 4 ? (int)threadIdx.x - 64 : (int)threadIdx.x - 384;
-    for (int c = 0; c < nch; ++c) {
-      const int sq = c % QST, skv = c % KVST;
-      const int b = c & 1;
-      const int L = min(kC, hi - lo - c * kC);
+    int gc = 0;
+    for (int it = 0; it < nitems; ++it) {
+     const WorkItem w = item(it);
+     load_table(pw_prep, w, it, pt, kPrep, 3);
+     const int nch = item_chunks(w);
+     for (int c = 0; c < nch; ++c, ++gc) {
+      const int sq = gc % QST, skv = gc % KVST;
+      const int b = gc & 1;
+      const int L = min(kC, w.hi - w.lo - c * kC);
       uint8_t* qs = smem + sq * G::QK_BYTES;
       uint8_t* ks = smem + G::OFF_KV + skv * G::KV_BYTES;
       uint8_t* vs = ks + G::QK_BYTES;
       uint8_t* klo = smem + G::OFF_KLO;
       uint8_t* qlo = smem + G::OFF_QLO + b * G::QK_BYTES;
-      mbar_wait(&full_kv[skv], (c / KVST) & 1);
+      mbar_wait(&full_kv[skv], (gc / KVST) & 1);
       if (!SO) {
-        mbar_wait(&full_q[sq], (c / QST) & 1);
-        if (c >= 2) mbar_wait(&derA_free[b], ((c >> 1) - 1) & 1);
-        if (c >= 1) mbar_wait(klo_free, (c - 1) & 1);
+        mbar_wait(&full_q[sq], (gc / QST) & 1);
+        if (gc >= 2) mbar_wait(&derA_free[b], ((gc >> 1) - 1) & 1);
+        if (gc >= 1) mbar_wait(klo_free, (gc - 1) & 1);
         // Klo, Qlo (and, with TF32_TRUNC_INPLACE, the hi parts truncated in place)
         for (int i = pt; i < 2 * G::QK_BYTES / 16; i += kPrep) {
           const bool isk = i < G::QK_BYTES / 16;
@@ -246,15 +310,12 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         fence_proxy_async_smem();
         mbar_arrive(&prepA[b]);
       }
-      if (c > 0) mbar_wait(derB_free, (c - 1) & 1);
+      if (gc > 0) mbar_wait(derB_free, (gc - 1) & 1);
       // Row units (a 128-byte row of one 32-column box): K' = gamma^(L-1-s) K (zero past the ragged
       // end) split into hi | lo, and V split into hi (in place) | lo -- both re-laid from the TMA's
       // 128B swizzle (16-byte chunk j of row r at j ^ (r & 7)) to the MN-major tf32 layout
       // (32-byte granule g at g ^ (r & 3)), the only MN-major layout kind::tf32 reads.
-      if (!SO && TF32_TRUNC_INPLACE) {
-        // K' reads K (truncated in place by the prepA pass, possibly by another thread) + Klo
-        named_bar_sync(3, kPrep);
-      }
+      if (!SO && TF32_TRUNC_INPLACE) named_bar_sync(5, kPrep);   // K' reads K truncated by other threads
       for (int u = pt; u < (G::KB + 4) * kC; u += kPrep) {
         const bool isv = u >= G::KB * kC;
         const int uu = isv ? u - G::KB * kC : u;
@@ -264,9 +325,9 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         float4 x[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) x[j] = *reinterpret_cast<const float4*>(src + ((j ^ (r & 7)) << 4));
-        float w = 1.f;
+        float wgt = 1.f;
         if (!isv) {
-          w = r < L ? pw[r < L ? L - 1 - r : 0] : 0.f;
+          wgt = r < L ? pw_prep[r < L ? L - 1 - r : 0] : 0.f;
           if (!SO && TF32_TRUNC_INPLACE) {   // K = hi + lo exactly
             const uint8_t* ls = klo + boff;
 #pragma unroll
@@ -283,7 +344,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         for (int jj = 0; jj < 8; ++jj) {
           const int j = jj ^ flip;
           float4 v4 = flip ? x[jj ^ 1] : x[jj], h, l;
-          v4.x *= w; v4.y *= w; v4.z *= w; v4.w *= w;
+          v4.x *= wgt; v4.y *= wgt; v4.z *= wgt; v4.w *= wgt;
           h.x = tf32_hi(v4.x); h.y = tf32_hi(v4.y); h.z = tf32_hi(v4.z); h.w = tf32_hi(v4.w);
           l.x = v4.x - h.x; l.y = v4.y - h.y; l.z = v4.z - h.z; l.w = v4.w - h.w;
           const int pos = ((((j >> 1) ^ (r & 3)) << 1) | (j & 1)) << 4;
@@ -292,8 +353,8 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
       }
       fence_proxy_async_smem();
-      if (dumping && c == 0) {   // raw smem of K, V (stage 0), K'hi, Vlo after prep: 4 x 4096 floats
-        named_bar_sync(3, kPrep);
+      if (dumping && gc == 0) {   // raw smem of K, V (stage 0), K'hi, Vlo after prep: 4 x 4096 floats
+        named_bar_sync(5, kPrep);
         for (int i = pt; i < 4096; i += kPrep) {
           dump[20480 + i] = i < G::QK_BYTES / 4 ? reinterpret_cast<const float*>(ks)[i] : 0.f;
           dump[24576 + i] = reinterpret_cast<const float*>(vs)[i];
@@ -302,6 +363,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
       }
       mbar_arrive(prepB);
+     }
     }
   } else if (warp < 12) {
     // ------------------------------------------------------------ running state + outputs
@@ -312,8 +374,8 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const int sub = (warp - 4) % 4;
     const int d = sub * 32 + (int)lane;
     const int col0 = g * SC;
-    const int jd = j0 + d;
-    const bool dv_ok = jd < dv;
+    const int sidx = (int)threadIdx.x - 128;
+    const bool leader = sidx == 0;
     const uint32_t lane_base = tbase + ((uint32_t)(sub * 32) << 16);
     float S[SC];
     auto publish = [&]() {
@@ -333,111 +395,161 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       tc_fence_before();
       mbar_arrive(st_full);
     };
-    // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs), 16 columns at a time
-    {
-      const float w_in = gpow(lg, (float)lo);
-      const bool in_ok = s_in != nullptr && dv_ok;
+    int gc = 0;
+    for (int it = 0; it < nitems; ++it) {
+      const WorkItem w = item(it);
+      const int jd = w.j0 + d;
+      const bool dv_ok = jd < dv;
+      const float lgi = log2g[w.bh % H];
+      load_table(pw_st, w, it, sidx, 256, 6);
+      if (w.in_slot >= 0) {
+        // balanced tail: the previous range's head published the state at lo (s_in included)
+        if (leader)
+          while (ld_acquire_gpu(bal.flags + w.in_slot) == 0u) __nanosleep(256);
+        named_bar_sync(6, 256);
+        const float* hp = bal.hst + (size_t)w.in_slot * dk * kDVT + d;
 #pragma unroll
-      for (int j = 0; j < SC; j += 16) {
+        for (int i = 0; i < SC; ++i) S[i] = (col0 + i < dk) ? __ldcg(hp + (size_t)(col0 + i) * kDVT) : 0.f;
+      } else {
+        // S_init = gamma^lo s_in + sum_{q: hi_q <= lo} gamma^(lo - hi_q) loc[q]  (SegArgs), 16 columns at a time
+        const float w_in = gpow(lgi, (float)w.lo);
+        const bool in_ok = s_in != nullptr && dv_ok;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int ci = col0 + j + i;
-          S[j + i] = (in_ok && ci < dk) ? w_in * __ldg(s_in + ((size_t)bh * dk + ci) * dv + jd) : 0.f;
+        for (int j = 0; j < SC; j += 16) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int ci = col0 + j + i;
+            S[j + i] = (in_ok && ci < dk) ? w_in * __ldg(s_in + ((size_t)w.bh * dk + ci) * dv + jd) : 0.f;
+          }
+          for (int qi = 0; qi < sa.nloc; ++qi) {
+            const float wq = seg_loc_weight(sa, qi, N, w.lo, lgi);
+            if (wq < 0.f || !dv_ok) continue;
+            const float* lq = sa.loc + qi * per_state + ((size_t)w.bh * dk + col0 + j) * dv + jd;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (col0 + j + i < dk) S[j + i] = fmaf(wq, __ldg(lq + (size_t)i * dv), S[j + i]);
+          }
         }
-        for (int qi = 0; qi < sa.nloc; ++qi) {
-          const float wq = seg_loc_weight(sa, qi, N, lo, lg);
-          if (wq < 0.f || !dv_ok) continue;
-          const float* lq = sa.loc + qi * per_state + ((size_t)bh * dk + col0 + j) * dv + jd;
+      }
+      const int nch = item_chunks(w);
+      if (!SO && nch > 0) publish();
+      float* orow = SO ? nullptr : o + ((size_t)w.bh * N + w.lo) * dv + jd;
+      for (int c = 0; c < nch; ++c, ++gc) {
+        const int L = min(kC, w.hi - w.lo - c * kC);
+        mbar_wait(mma_s_bar, gc & 1);
+        tc_fence_after();
+        const float carry = pw_st[L];
+#pragma unroll
+        for (int j = 0; j < SC / 16; ++j) {
+          float ds[16];
+          tmem_ld16(lane_base + T_DS + col0 + 16 * j, ds);
+          tmem_wait_ld();
+          if (dumping && gc == 0)
+            for (int i = 0; i < 16; ++i) dump[2048 + d * 128 + col0 + 16 * j + i] = ds[i];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) S[16 * j + i] = fmaf(carry, S[16 * j + i], ds[i]);
+        }
+        tc_fence_before();
+        mbar_arrive(ds_free);
+        if (SO) continue;
+        mbar_wait(mma_o_bar, gc & 1);                 // Oi, Ox done: S hi/lo may be replaced
+        tc_fence_after();
+        if (c != nch - 1) publish();
+        // ---- outputs: O[t][d] = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t], tokens g*16 .. g*16+15;
+        //      for each t the 32 lanes of a warp store 32 consecutive dv columns (128 B)
+        float ov[16], xv[16];
+        tmem_ld16(lane_base + T_O + g * 16, ov);
+        tmem_ld16(lane_base + T_OX + g * 16, xv);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(o_free);
+        if (dv_ok) {
+          float* orc = orow + (size_t)(c * kC + g * 16) * dv;
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (col0 + j + i < dk) S[j + i] = fmaf(wq, __ldg(lq + (size_t)i * dv), S[j + i]);
+            if (g * 16 + i < L) __stcs(orc + (size_t)i * dv, fmaf(pw_st[g * 16 + i + 1], xv[i], ov[i]));
         }
       }
-    }
-    if (!SO && nch > 0) publish();
-    float* orow = SO ? nullptr : o + ((size_t)bh * N + lo) * dv + jd;
-    for (int c = 0; c < nch; ++c) {
-      const int L = min(kC, hi - lo - c * kC);
-      mbar_wait(mma_s_bar, c & 1);
-      tc_fence_after();
-      const float carry = pw[L];
+      // end state: a balanced head publishes it to its hand-off slot; otherwise state-only
+      // launches write one local state per segment and full launches only the segment ending
+      // the sequence (its seed already covers every earlier token)
+      if (w.out_slot >= 0) {
+        float* hp = bal.hst + (size_t)w.out_slot * dk * kDVT + d;
 #pragma unroll
-      for (int j = 0; j < SC / 16; ++j) {
-        float ds[16];
-        tmem_ld16(lane_base + T_DS + col0 + 16 * j, ds);
-        tmem_wait_ld();
-        if (dumping && c == 0)
-          for (int i = 0; i < 16; ++i) dump[2048 + d * 128 + col0 + 16 * j + i] = ds[i];
+        for (int i = 0; i < SC; ++i)
+          if (col0 + i < dk) hp[(size_t)(col0 + i) * kDVT] = S[i];
+        __threadfence();
+        named_bar_sync(7, 256);
+        if (leader) st_release_gpu(bal.flags + w.out_slot, 1u);
+      } else if (s_out && dv_ok && (BAL ? w.hi == N : (SO || blockIdx.z == gridDim.z - 1))) {
+        float* so = s_out + (SO ? blockIdx.z * per_state : 0) + (size_t)w.bh * dk * dv + jd;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) S[16 * j + i] = fmaf(carry, S[16 * j + i], ds[i]);
+        for (int i = 0; i < SC; ++i)
+          if (col0 + i < dk) so[(size_t)(col0 + i) * dv] = S[i];
       }
-      tc_fence_before();
-      mbar_arrive(ds_free);
-      if (SO) continue;
-      mbar_wait(mma_o_bar, c & 1);                 // Oi, Ox done: S hi/lo may be replaced
-      tc_fence_after();
-      if (c != nch - 1) publish();
-      // ---- outputs: O[t][d] = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t], tokens g*16 .. g*16+15;
-      //      for each t the 32 lanes of a warp store 32 consecutive dv columns (128 B)
-      float ov[16], xv[16];
-      tmem_ld16(lane_base + T_O + g * 16, ov);
-      tmem_ld16(lane_base + T_OX + g * 16, xv);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(o_free);
-      if (dv_ok) {
-        float* orc = orow + (size_t)(c * kC + g * 16) * dv;
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (g * 16 + i < L) __stcs(orc + (size_t)i * dv, fmaf(pw[g * 16 + i + 1], xv[i], ov[i]));
-      }
-    }
-    // end state: state-only launches write one local state per segment, full launches only the
-    // segment ending the sequence (its seed already covers every earlier token)
-    if (s_out && dv_ok && (SO || blockIdx.z == gridDim.z - 1)) {
-      float* so = s_out + (SO ? blockIdx.z * per_state : 0) + (size_t)bh * dk * dv + jd;
-#pragma unroll
-      for (int i = 0; i < SC; ++i)
-        if (col0 + i < dk) so[(size_t)(col0 + i) * dv] = S[i];
     }
   } else if (warp == 12) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      for (int c = 0; c < nch; ++c) {
-        const int sq = c % QST, skv = c % KVST;
-        const int t0 = lo + c * kC;
-        // warm L2 with the chunk that will reuse this K|V stage, so its load is an L2 hit
-        if (c + KVST < nch) {
-          const int tp = t0 + KVST * kC;
+      // L2-prefetch cursor over the work list's chunk stream, KVST chunks ahead of the loads
+      struct Cursor { int it, c; WorkItem w; };
+      auto settle = [&](Cursor& u) {
+        while (u.it < nitems && u.c >= item_chunks(u.w)) {
+          ++u.it;
+          u.c = 0;
+          if (u.it < nitems) u.w = item(u.it);
+        }
+      };
+      Cursor pf{0, 0, WorkItem{}};
+      if (nitems > 0) pf.w = item(0);
+      settle(pf);
+      for (int i = 0; i < KVST && pf.it < nitems; ++i) {
+        ++pf.c;
+        settle(pf);
+      }
+      int gc = 0;
+      for (int it = 0; it < nitems; ++it) {
+        const WorkItem w = item(it);
+        const int nch = item_chunks(w);
+        for (int c = 0; c < nch; ++c, ++gc) {
+          const int sq = gc % QST, skv = gc % KVST;
+          const int t0 = w.lo + c * kC;
+          // warm L2 with the chunk that will reuse this K|V stage, so its load is an L2 hit
+          if (TF32_L2_PREFETCH && pf.it < nitems) {
+            const int tp = pf.w.lo + pf.c * kC;
 #pragma unroll
-          for (int kb = 0; kb < G::KB; ++kb) {
-            if (!SO) tma_prefetch_l2_3d(&tm_q, kb * 32, tp, bh);
-            tma_prefetch_l2_3d(&tm_k, kb * 32, tp, bh);
+            for (int kb = 0; kb < G::KB; ++kb) {
+              if (!SO) tma_prefetch_l2_3d(&tm_q, kb * 32, tp, pf.w.bh);
+              tma_prefetch_l2_3d(&tm_k, kb * 32, tp, pf.w.bh);
+            }
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) tma_prefetch_l2_3d(&tm_v, pf.w.j0 + nb * 32, tp, pf.w.bh);
+            ++pf.c;
+            settle(pf);
           }
+          if (!SO) {
+            mbar_wait(&empty_q[sq], ((gc / QST) & 1) ^ 1);
+            uint8_t* qd = smem + sq * G::QK_BYTES;
+            mbar_arrive_expect_tx(&full_q[sq], G::QK_BYTES);
 #pragma unroll
-          for (int nb = 0; nb < 4; ++nb) tma_prefetch_l2_3d(&tm_v, j0 + nb * 32, tp, bh);
+            for (int kb = 0; kb < G::KB; ++kb) tma_load_3d(qd + kb * 4096, &tm_q, &full_q[sq], kb * 32, t0, w.bh);
+          }
+          mbar_wait(&empty_kv[skv], ((gc / KVST) & 1) ^ 1);
+          uint8_t* kd = smem + G::OFF_KV + skv * G::KV_BYTES;
+          mbar_arrive_expect_tx(&full_kv[skv], G::KV_BYTES);
+#pragma unroll
+          for (int kb = 0; kb < G::KB; ++kb) tma_load_3d(kd + kb * 4096, &tm_k, &full_kv[skv], kb * 32, t0, w.bh);
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb)
+            tma_load_3d(kd + G::QK_BYTES + nb * 4096, &tm_v, &full_kv[skv], w.j0 + nb * 32, t0, w.bh);
         }
-        if (!SO) {
-          mbar_wait(&empty_q[sq], ((c / QST) & 1) ^ 1);
-          uint8_t* qd = smem + sq * G::QK_BYTES;
-          mbar_arrive_expect_tx(&full_q[sq], G::QK_BYTES);
-#pragma unroll
-          for (int kb = 0; kb < G::KB; ++kb) tma_load_3d(qd + kb * 4096, &tm_q, &full_q[sq], kb * 32, t0, bh);
-        }
-        mbar_wait(&empty_kv[skv], ((c / KVST) & 1) ^ 1);
-        uint8_t* kd = smem + G::OFF_KV + skv * G::KV_BYTES;
-        mbar_arrive_expect_tx(&full_kv[skv], G::KV_BYTES);
-#pragma unroll
-        for (int kb = 0; kb < G::KB; ++kb) tma_load_3d(kd + kb * 4096, &tm_k, &full_kv[skv], kb * 32, t0, bh);
-#pragma unroll
-        for (int nb = 0; nb < 4; ++nb)
-          tma_load_3d(kd + G::QK_BYTES + nb * 4096, &tm_v, &full_kv[skv], j0 + nb * 32, t0, bh);
       }
     }
   } else {
     // ------------------------------------------------------------ MMA issuer (whole warp)
     // per chunk: dS(c) -> Oi(c) -> MMA1(c+1) -> Ox(c); MMA1 runs ahead so the mask epilogue of
-    // c+1 overlaps the state publish that Ox(c) waits for
+    // c+1 overlaps the state publish that Ox(c) waits for.  The tensor pipe sees one flat chunk
+    // stream across the work list (only buffer/stage indices depend on the chunk).
     constexpr uint32_t id_qk = idesc_tf32(64, kC, false, false);     // P^T = K Q^T (M = 64)
     constexpr uint32_t id_vk = idesc_tf32(128, DKP, true, true);     // dS^T = V^T K'
     constexpr uint32_t id_vp = idesc_tf32(128, kC, true, true);      // Oi^T = V^T P^T
@@ -451,6 +563,12 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const uint64_t kph_m = dM0 + (G::OFF_KPH >> 4), kpl_m = dM0 + (G::OFF_KPL >> 4);
     const uint64_t vlo_m = dM0 + (G::OFF_VLO >> 4);
     const uint64_t ph_m = dM0 + (G::OFF_P >> 4), pl_m = ph_m + (4096 >> 4);
+    int nchunks = 0;
+    for (int it = 0; it < nitems; ++it) nchunks += item_chunks(item(it));
+    // a lane-0 broadcast makes the chunk count (and every descriptor derived from the chunk
+    // index) provably warp-uniform: ptxas keeps them in uniform registers instead of wrapping each
+    // tcgen05.mma in a per-lane R2UR loop
+    nchunks = __shfl_sync(0xffffffffu, nchunks, 0);
     auto issue_mma1 = [&](int c) {
       const uint64_t q_k = dK0 + (c % QST) * kQK, k_k = kv_k0 + (c % KVST) * kKV;
       const uint64_t qlo_k = qlo_k0 + (c & 1) * kQK;
@@ -471,8 +589,8 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       mma_commit_elect(mma1_bar);
       mma_commit_elect(klo_free);
     };
-    if (!SO && nch > 0) issue_mma1(0);
-    for (int c = 0; c < nch; ++c) {
+    if (!SO && nchunks > 0) issue_mma1(0);
+    for (int c = 0; c < nchunks; ++c) {
       const int sq = c % QST, skv = c % KVST;
       const uint64_t q_k = dK0 + sq * kQK;                            // raw Q (hi), K-major
       const uint64_t qlo_k = qlo_k0 + (c & 1) * kQK;
@@ -505,7 +623,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         mma_commit_elect(p_free);
         mma_commit_elect(derB_free);
         mma_commit_elect(&empty_kv[skv]);            // K (MMA1, K') and V (dS, Oi) consumed
-        if (c + 1 < nch) issue_mma1(c + 1);
+        if (c + 1 < nchunks) issue_mma1(c + 1);
         mbar_wait(st_full, c & 1);
         tc_fence_after();
         // Ox^T = Shi Qhi + Shi Qlo + Slo Qhi   (A from TMEM: 8 columns per K step)
@@ -551,9 +669,10 @@ bool make_map_f32(CUtensorMap* map, const void* base, int64_t D, int64_t N, int6
   return r == CUDA_SUCCESS;
 }
 
-template <int DKP, int QST, int KVST, bool SO>
+template <int DKP, int QST, int KVST, bool SO, bool BAL = false>
 cudaError_t launch_v4(const void* q, const void* k, const void* v, void* o, const float* log2g, const float* s_in,
-                      float* s_out, const ShapeArgs& s, const SegArgs& sa, int nz, cudaStream_t stream) {
+                      float* s_out, const ShapeArgs& s, const SegArgs& sa, int nz, cudaStream_t stream,
+                      const Balance& bal = Balance{}, int ctas = 0) {
   using G = v4::Cfg<DKP, QST, KVST>;
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
   const int64_t BH = s.B * s.H;
@@ -561,13 +680,20 @@ cudaError_t launch_v4(const void* q, const void* k, const void* v, void* o, cons
   if (!make_map_f32(&mk, k, s.dk, s.N, BH) || !make_map_f32(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
   mq = mk;
   if (!SO && !make_map_f32(&mq, q, s.dk, s.N, BH)) return cudaErrorInvalidValue;
-  auto kern = v4::prefill_tf32_kernel<DKP, QST, KVST, SO>;
+  auto kern = v4::prefill_tf32_kernel<DKP, QST, KVST, SO, BAL>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
-  const dim3 grid((unsigned)((s.dv + v4::kDVT - 1) / v4::kDVT), (unsigned)BH, (unsigned)nz);
-  err = launch_pdl(kern, grid, dim3(v4::kThreads), G::SMEM, stream, mq, mk, mv, static_cast<float*>(o), log2g,
-                   s_in, s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, sa, g_tf32_dump);
-  if (err != cudaSuccess) return err;
+  if constexpr (BAL && !TF32_BAL_PDL) {   // follows the memset of its flags: plain stream order
+    kern<<<dim3((unsigned)ctas), v4::kThreads, G::SMEM, stream>>>(mq, mk, mv, static_cast<float*>(o), log2g, s_in,
+                                                                  s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv,
+                                                                  sa, bal, nullptr);
+  } else {
+    const dim3 grid = BAL ? dim3((unsigned)ctas)
+                          : dim3((unsigned)((s.dv + v4::kDVT - 1) / v4::kDVT), (unsigned)BH, (unsigned)nz);
+    err = launch_pdl(kern, grid, dim3(v4::kThreads), G::SMEM, stream, mq, mk, mv, static_cast<float*>(o), log2g,
+                     s_in, s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, sa, bal, g_tf32_dump);
+    if (err != cudaSuccess) return err;
+  }
   count_launch();
   return cudaGetLastError();
 }
@@ -607,6 +733,52 @@ cudaError_t launch_prefill_tf32(const void* q, const void* k, const void* v, voi
                       : launch_v4<64, 4, 4, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
   return state_only ? launch_v4<128, 3, 2, true>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream)
                     : launch_v4<128, 3, 2, false>(q, k, v, o, log2g, s_in, s_out, s, sa, nz, stream);
+}
+
+int tf32_balance_ctas(const ShapeArgs& s, int sms) {
+  // one CTA per SM over equal chunk ranges when the (b, h, 128-wide dv tile) units do not fill whole
+  // waves: the kernel is tensor-pipe bound, so a partly filled last wave idles SMs outright
+  const int64_t units = s.B * s.H * ((s.dv + v4::kDVT - 1) / v4::kDVT), nc = (s.N + v4::kC - 1) / v4::kC;
+  if (units <= sms || units % sms == 0 || units * nc > (1LL << 31) - 1) return 0;
+  // measured (B200): 149 units x 8192 tokens 1.41 -> 0.87 ms balanced; configs[1] (256 units,
+  // 1.73 waves) gains nothing (1.488 both: per-chunk time rises with the number of busy SMs, so
+  // the light second wave of the plain grid already runs faster), hence the margin
+  const double plain = (double)((units + sms - 1) / sms) * (double)nc;
+  const double bal = (double)((units * nc + sms - 1) / sms);
+  return bal < 0.8 * plain ? sms : 0;
+}
+
+size_t tf32_balance_workspace_bytes(const ShapeArgs& s, int ctas) {
+  return 256 * (size_t)((ctas + 1 + 63) / 64) + (size_t)ctas * s.dk * v4::kDVT * sizeof(float);
+}
+
+cudaError_t launch_prefill_tf32_balanced(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                                         const float* s_in, float* s_out, const ShapeArgs& s, int ctas, void* ws,
+                                         cudaStream_t stream) {
+  for (const void* p : {q, k, v, (const void*)o})
+    if (reinterpret_cast<uintptr_t>(p) & 15) return cudaErrorNotSupported;
+  if (!tf32_supported(s, LINATTN_F32)) return cudaErrorNotSupported;
+  const int64_t ntiles = (s.dv + v4::kDVT - 1) / v4::kDVT;
+  const int64_t units = s.B * s.H * ntiles, nc = (s.N + v4::kC - 1) / v4::kC;
+  const int64_t w = (units * nc + ctas - 1) / ctas;
+  if (w < nc || units * nc > (1LL << 31) - 1) return cudaErrorNotSupported;
+  Balance bal;
+  bal.on = 1;
+  bal.units = (int)units;
+  bal.nc = (int)nc;
+  bal.w = (int)w;
+  bal.ntiles = (int)ntiles;
+  bal.chunk = v4::kC;
+  bal.tile = v4::kDVT;
+  bal.flags = static_cast<unsigned*>(ws);
+  bal.hst = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256 * (size_t)((ctas + 1 + 63) / 64));
+  const int used = (int)((units * nc + w - 1) / w);
+  cudaError_t err = cudaMemsetAsync(ws, 0, sizeof(unsigned) * (ctas + 1), stream);
+  if (err != cudaSuccess) return err;
+  const SegArgs sa{};
+  if (s.dk <= 32) return launch_v4<32, 4, 5, false, true>(q, k, v, o, log2g, s_in, s_out, s, sa, 1, stream, bal, used);
+  if (s.dk <= 64) return launch_v4<64, 4, 4, false, true>(q, k, v, o, log2g, s_in, s_out, s, sa, 1, stream, bal, used);
+  return launch_v4<128, 3, 2, false, true>(q, k, v, o, log2g, s_in, s_out, s, sa, 1, stream, bal, used);
 }
 
 }  // namespace linattn

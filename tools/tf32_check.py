@@ -32,6 +32,16 @@ for (B, H, N, dk, dv, seed) in [(1, 1, 32, 32, 128, 0), (1, 2, 100, 64, 64, 1), 
     worst = max(worst, err, serr, sperr)
     print(f"B={B} H={H} N={N} dk={dk} dv={dv}: out {err:.2e} s_out {serr:.2e} state_pass {sperr:.2e}", flush=True)
 print("worst", worst)
+# more (b, h) units than SMs with a partly filled last wave: balanced persistent launch
+for (B, H, N, dk, dv) in [(1, 150, 300, 64, 128), (2, 100, 257, 128, 128), (1, 160, 1000, 32, 256)]:
+    b, c, v = orc.gen_inputs(B, H, N, dk, dv, np.float32, 9)
+    gam = [[0.0, 0.9, 0.99, 1.0, 0.5][h % 5] for h in range(H)]
+    ref, ref_s = orc.seeded_blocked_attn(b, c, v, gam, True)
+    t = [torch.from_numpy(x).to(dev) for x in (b, c, v)]
+    s_out = torch.zeros(B, H, dk, dv, device=dev)
+    out = ops.prefill(*t, ops.log2_gamma(gam, True, dev), kernel="tf32", s_out=s_out)
+    print(f"balanced B={B} H={H} N={N} dk={dk} dv={dv}: out {orc.max_rel_error(out.cpu().numpy(), ref):.2e} "
+          f"s_out {orc.max_rel_error(s_out.cpu().numpy(), ref_s):.2e}", flush=True)
 
 B, H, N, d = 8, 32, 8192, 128
 g = torch.Generator(device=dev).manual_seed(0)
