@@ -435,9 +435,10 @@ def bench_cfg3(args, ops, dev, g, hbm, tc_burst, barrier, max_over_ranks):
             "kernel": "prefill_tc (dk=256: state in TMEM)"}
 
 
-def bench_fp32(args, ops, dev, g, hbm, barrier, max_over_ranks):
+def bench_fp32(args, ops, dev, g, hbm, tc_burst, barrier, max_over_ranks):
     """configs[1] shape in fp32 -- the reference's own arithmetic type: the fp32 parity mode
-    (FFMA kernel, <= 1e-4 vs the f64 oracle), the default route for fp32 inputs."""
+    (<= 1e-4 vs the f64 oracle), 3xTF32 on the tensor cores (the default route for fp32 inputs),
+    with the FFMA kernel it replaced timed beside it."""
     import torch
     B, H, N, d = 8, 32, 8192, 128
     q = torch.randn(B, H, N, d, device=dev, dtype=torch.float32, generator=g)
@@ -445,19 +446,23 @@ def bench_fp32(args, ops, dev, g, hbm, barrier, max_over_ranks):
     v = torch.randn(B, H, N, d, device=dev, dtype=torch.float32, generator=g)
     out = torch.empty_like(v)
     l2 = ops.log2_gamma(gammas(H), True, dev)
-    ms = _time_events(lambda: ops.prefill(q, k, v, l2, out=out, kernel="simt"), 5, barrier, max_over_ranks)
-    # FFMA work the kernel issues per (token, head) at chunk 32 and 64-wide dv tiles (two tiles):
-    # Q.K over the causal half of each chunk, A.V, Q.S, and the K^T V state update
-    fma = B * H * N * (2 * (17 * d) + 2 * (17 * 64) + 2 * (d * 64) + 2 * (d * 64))
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = sms * 128 * 2 * 1.965e9 / 1e12          # FP32 FFMA TFLOP/s at the 1965 MHz max clock
-    tf = 2 * fma / (ms * 1e-3) / 1e12
+    ms = _time_events(lambda: ops.prefill(q, k, v, l2, out=out, kernel="auto"), 10, barrier, max_over_ranks)
+    ms_simt = _time_events(lambda: ops.prefill(q, k, v, l2, out=out, kernel="simt"), 3, barrier, max_over_ranks)
+    nbytes = B * H * N * 4 * 4 * d
+    # tcgen05 kind::tf32 flops issued per 32-token chunk and 128-wide dv tile, 3 products each:
+    # MMA1 at M = 64 (K = dk), dS^T (N = dk, K = 32), O_intra (N = 32, K = 32), O_inter (N = 32, K = dk)
+    per_chunk = 3 * 2 * (64 * 32 * d + 128 * d * 32 + 128 * 32 * 32 + 128 * 32 * d)
+    tf_exec = B * H * (N // 32) * per_chunk / (ms * 1e-3) / 1e12
+    tf32_peak = tc_burst / 2        # kind::tf32 issues K = 8 per MMA at the kind::f16 rate (K = 16)
     del q, k, v, out
     return {"workload": "configs[1] shape B=8,H=32,N=8192,d=128 in fp32 (b200-chunked-f32)",
             "ms_per_step": ms, "tokens_per_s": B * N / (ms * 1e-3),
-            "hbm_gbs": B * H * N * 4 * 4 * d / (ms * 1e-3) / 1e9,
-            "ffma_tflops_issued": tf, "ffma_frac_of_peak": tf / peak, "ffma_peak_tflops": peak,
-            "kernel": "prefill_simt (fp32 FFMA, cp.async staging, balanced schedule)"}
+            "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "frac_of_hbm": nbytes / (ms * 1e-3) / 1e9 / hbm,
+            "bytes_per_step": nbytes,
+            "tf32_tflops_executed": tf_exec, "tf32_frac_executed_of_peak": tf_exec / tf32_peak,
+            "tf32_peak_tflops": tf32_peak, "tf32_peak_kind": "measured bf16 burst / 2",
+            "kernel": ops.prefill_kernel_name(d, d, torch.float32) + " (3xTF32 tcgen05 kind::tf32)",
+            "ffma_kernel_ms": ms_simt}
 
 
 def bench_seqpar(args, ops, dev, g, hbm, world, rank, barrier, max_over_ranks):
@@ -612,7 +617,7 @@ def run_ours(args):
     # split inside the GPU at N=1, sequence parallel over the ranks (one NCCL all-gather) at N>1
     cfg3 = None if args.no_extra else bench_cfg3(args, ops, dev, g, hbm, tc_burst, barrier, max_over_ranks)
     cfg5 = None if args.no_extra else bench_seqpar(args, ops, dev, g, hbm, world, rank, barrier, max_over_ranks)
-    f32 = None if args.no_extra else bench_fp32(args, ops, dev, g, hbm, barrier, max_over_ranks)
+    f32 = None if args.no_extra else bench_fp32(args, ops, dev, g, hbm, tc_burst, barrier, max_over_ranks)
 
     # CPU baseline: the reference's own CPU route (baseline/_ref), rank 0 at N=1 only, ~10 s
     cpu = None

@@ -480,7 +480,10 @@ def test_random_shapes_fuzz(la, seed):
     s0 = rng.standard_normal((B, H, dk, dv)).astype(np.float32) * 0.05
     ref, ref_s = orc.seeded_blocked_attn(b, c, v, gam, True, s0.astype(np.float64), block=64)
     l2 = ops.log2_gamma(gam, True, "cuda")
-    for dt, kernel, tol in ((torch.bfloat16, "auto", TOL_BF16), (torch.float32, "simt", TOL_F32)):
+    legs = [(torch.bfloat16, "auto", TOL_BF16), (torch.float32, "simt", TOL_F32)]
+    if dk <= 128 and dk % 4 == 0 and dv % 4 == 0:
+        legs.append((torch.float32, "tf32", TOL_F32))      # the 3xTF32 tensor-core parity mode
+    for dt, kernel, tol in legs:
         s_out = torch.full((B, H, dk, dv), float("nan"), device="cuda")
         out = ops.prefill(dev(b, dt), dev(c, dt), dev(v, dt), l2, s_in=dev(s0), s_out=s_out, kernel=kernel)
         assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= tol, (dt, B, H, N, dk, dv)

@@ -62,17 +62,17 @@ def test_auto_split_matches_oracle(ops, dk, dv):
 
 
 @pytest.mark.parametrize("seg_len,m", [(256, 1), (256, 2), (256, 3), (512, 4), (64, 1)])
-@pytest.mark.parametrize("mode", ["tc", "simt"])
+@pytest.mark.parametrize("mode", ["tc", "simt", "tf32"])
 def test_segmented_geometries(ops, seg_len, m, mode):
     """Ragged N, empty sub-segments (256/3 -> 128+128+0), s_in seeding and the end state."""
-    B, H, N, d = 2, 3, 1000, 128 if mode == "tc" else 64
+    B, H, N, d = 2, 3, 1000, 64 if mode == "simt" else 128
     gam = [0.0, 0.97, 1.0]
     b, c, v = orc.gen_inputs(B, H, N, d, d, np.float32, 32)
     b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
     s0 = np.random.default_rng(5).standard_normal((B, H, d, d)).astype(np.float32) * 0.1
     ref, ref_s = orc.seeded_blocked_attn(b, c, v, gam, True, s0.astype(np.float64), block=64)
     dt, tol = (torch.bfloat16, TOL_BF16) if mode == "tc" else (torch.float32, TOL_F32)
-    kernel = "tc" if mode == "tc" else "simt"
+    kernel = mode
     l2 = ops.log2_gamma(gam, True, "cuda")
     q, k, vv = dev(b, dt), dev(c, dt), dev(v, dt)
     nseg = -(-N // seg_len)
@@ -234,17 +234,20 @@ def test_balanced_schedule(ops, B, H, dk, dv, N):
     assert torch.equal(again, out)
 
 
-@pytest.mark.parametrize("B,H,N,dk,dv", [(3, 53, 300, 128, 128), (2, 80, 1000, 64, 96), (1, 150, 65, 32, 64)])
-def test_balanced_schedule_fp32(ops, B, H, N, dk, dv):
-    """The FFMA kernel's balanced persistent schedule (more 64-wide units than resident CTAs):
-    fp32 parity with s_in seeding and s_out at the 1e-4 bar."""
+@pytest.mark.parametrize("kernel", ["simt", "tf32"])
+@pytest.mark.parametrize("B,H,N,dk,dv", [(3, 53, 300, 128, 128), (2, 80, 1000, 64, 96), (1, 150, 65, 32, 64),
+                                         (1, 149, 2000, 128, 128)])
+def test_balanced_schedule_fp32(ops, B, H, N, dk, dv, kernel):
+    """The balanced persistent schedules of the fp32 kernels (FFMA: more 64-wide units than
+    resident CTAs; 3xTF32: more 128-wide units than SMs with a poorly filled last wave): fp32
+    parity with s_in seeding and s_out at the 1e-4 bar."""
     gam = [0.0, 1.0] + [1 - 2.0 ** (-3 - (h % 12)) for h in range(H - 2)]
     b, c, v = orc.gen_inputs(B, H, N, dk, dv, np.float32, 60 + N)
     s0 = np.random.default_rng(N).standard_normal((B, H, dk, dv)).astype(np.float32) * 0.05
     ref, ref_s = orc.seeded_blocked_attn(b, c, v, gam, True, s0.astype(np.float64), block=64)
     l2 = ops.log2_gamma(gam, True, "cuda")
     s_out = torch.full((B, H, dk, dv), float("nan"), device="cuda")
-    out = ops.prefill(dev(b), dev(c), dev(v), l2, s_in=dev(s0), s_out=s_out, kernel="simt")
+    out = ops.prefill(dev(b), dev(c), dev(v), l2, s_in=dev(s0), s_out=s_out, kernel=kernel)
     assert orc.max_rel_error(out.cpu().numpy(), ref) <= TOL_F32
     assert orc.max_rel_error(s_out.cpu().numpy(), ref_s) <= TOL_F32
 
@@ -273,15 +276,14 @@ def test_batch_heads_beyond_grid_limit(ops):
         assert orc.max_rel_error(rec[2099:].float().cpu().numpy(), ref) <= (TOL_F32 if dt == torch.float32 else TOL_BF16)
 
 
-@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
-def test_state_pass_split(ops, dt):
+@pytest.mark.parametrize("dt,kernel", [(torch.bfloat16, "auto"), (torch.float32, "simt"), (torch.float32, "tf32")])
+def test_state_pass_split(ops, dt, kernel):
     """Few (b, h) units: the state pass runs every segment in parallel and scans them (the same
     plan as the prefill split); the end state matches the oracle and the unsplit prefill's s_out."""
     gam = [0.0, 0.97, 1 - 2.0 ** -12]
     b, c, v = orc.gen_inputs(1, 3, 5000, 128, 128, np.float32, 77)
     b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
     l2 = ops.log2_gamma(gam, True, "cuda")
-    kernel = "auto" if dt == torch.bfloat16 else "simt"
     assert ops.seq_plan(1, 3, 5000, 128, 128, dt, kernel)[1] > 1
     s = ops.state_pass(dev(c, dt), dev(v, dt), l2, kernel=kernel)
     ref = np.stack([[orc.segment_end_state(c[0, h], v[0, h], gam[h]) for h in range(3)]])
@@ -305,7 +307,7 @@ def test_sp_fuzz(ops, seed):
     bounds = list(zip([0] + cuts.tolist(), cuts.tolist() + [N]))
     gam = [float(rng.choice([0.0, 0.9, 1 - 2.0 ** -10, 1.0])) for _ in range(H)]
     fp32 = bool(rng.integers(0, 2)) and dk <= 128
-    dt, tol, kernel = (torch.float32, TOL_F32, "simt") if fp32 else (torch.bfloat16, TOL_BF16, "auto")
+    dt, tol, kernel = (torch.float32, TOL_F32, ["simt", "tf32"][seed % 2]) if fp32 else (torch.bfloat16, TOL_BF16, "auto")
     b, c, v = orc.gen_inputs(B, H, N, dk, dv, np.float32, 800 + seed)
     if not fp32:
         b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
