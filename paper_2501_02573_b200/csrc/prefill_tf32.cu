@@ -40,6 +40,9 @@
 #ifndef TF32_BAL_ONEITEM
 #define TF32_BAL_ONEITEM 0     // dev bisect: balance_item items, but a compile-time item count of 1
 #endif
+#ifndef TF32_V_ATOM32
+#define TF32_V_ATOM32 0        // TMA writes V in the 32B-granule swizzle (CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
+#endif
 #ifndef TF32_BAL_PLAINITEM
 #define TF32_BAL_PLAINITEM 0   // dev bisect: BAL instantiation with the plain one-unit-per-CTA items
 #endif
@@ -316,7 +319,17 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       // 128B swizzle (16-byte chunk j of row r at j ^ (r & 7)) to the MN-major tf32 layout
       // (32-byte granule g at g ^ (r & 3)), the only MN-major layout kind::tf32 reads.
       if (!SO && TF32_TRUNC_INPLACE) named_bar_sync(5, kPrep);   // K' reads K truncated by other threads
-      for (int u = pt; u < (G::KB + 4) * kC; u += kPrep) {
+      if (TF32_V_ATOM32) {   // V already in the MN-major tf32 layout: Vlo at the same positions
+        for (int i = pt; i < G::V_BYTES / 16; i += kPrep) {
+          float4* src = reinterpret_cast<float4*>(vs + i * 16);
+          float4 x = *src, h, l;
+          h.x = tf32_hi(x.x); h.y = tf32_hi(x.y); h.z = tf32_hi(x.z); h.w = tf32_hi(x.w);
+          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+          *reinterpret_cast<float4*>(smem + G::OFF_VLO + i * 16) = l;
+          if (TF32_TRUNC_INPLACE) *src = h;
+        }
+      }
+      for (int u = pt; u < (G::KB + (TF32_V_ATOM32 ? 0 : 4)) * kC; u += kPrep) {
         const bool isv = u >= G::KB * kC;
         const int uu = isv ? u - G::KB * kC : u;
         const int r = uu & (kC - 1);
@@ -656,7 +669,8 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 }  // namespace v4
 
 // [BH][N][D] fp32 viewed as a 3-D tensor (D fastest); boxes of 32 x 32, 128B swizzle.
-bool make_map_f32(CUtensorMap* map, const void* base, int64_t D, int64_t N, int64_t BH) {
+bool make_map_f32(CUtensorMap* map, const void* base, int64_t D, int64_t N, int64_t BH,
+                  CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = tf32_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)N, (cuuint64_t)BH};
@@ -664,7 +678,7 @@ bool make_map_f32(CUtensorMap* map, const void* base, int64_t D, int64_t N, int6
   cuuint32_t box[3] = {32, 32, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -677,7 +691,12 @@ cudaError_t launch_v4(const void* q, const void* k, const void* v, void* o, cons
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
   const int64_t BH = s.B * s.H;
   CUtensorMap mq, mk, mv;
-  if (!make_map_f32(&mk, k, s.dk, s.N, BH) || !make_map_f32(&mv, v, s.dv, s.N, BH)) return cudaErrorInvalidValue;
+  // V is only ever an MN-major operand: with TF32_V_ATOM32 the TMA writes it straight into the
+  // 32-byte-granule swizzle kind::tf32 reads (no relayout pass)
+  if (!make_map_f32(&mk, k, s.dk, s.N, BH) ||
+      !make_map_f32(&mv, v, s.dv, s.N, BH,
+                    TF32_V_ATOM32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
   mq = mk;
   if (!SO && !make_map_f32(&mq, q, s.dk, s.N, BH)) return cudaErrorInvalidValue;
   auto kern = v4::prefill_tf32_kernel<DKP, QST, KVST, SO, BAL>;
