@@ -39,8 +39,9 @@ from .errors import LinAttnError, UsageError
 from .tensor import AttnInputs, validate_inputs
 
 DEFAULT_MEM_CAP = 2 << 30  # kept for signature parity with the reference (oracle.py:16)
-TC_CHUNK = 64      # token chunk of the tensor-core kernel
-SIMT_CHUNK = 32    # token chunk of the fp32 FFMA kernel
+TC_CHUNK = 64      # token chunk of the bf16 tensor-core kernel (the reference default, kernels.py:57)
+TF32_CHUNK = 32    # token chunk of the 3xTF32 tensor-core kernel (fp32 parity mode)
+SIMT_CHUNK = 32    # token chunk of the FFMA kernel
 
 REFERENCE_ONLY = ("vanilla", "row-based", "block-based", "recursion", "two-level-block",
                   "fleet", "fleet-tiled")
@@ -73,12 +74,15 @@ CONCRETE_METHODS = [m for m in MethodId if m is not MethodId.AUTO]
 class BlockParams:
     """Tuning knobs (reference kernels.py:47-61 plus ``seq_parts``).
 
-    ``block_size``/``row_block``/``col_block``/``term_size``/``mem_cap`` are
-    accepted for signature parity; the device kernels use their native chunk
-    (TC_CHUNK / SIMT_CHUNK), which is what the reported opcount assumes.
-    Results are block-size invariant up to the dtype tolerance, as the
-    reference's are (test_kernels.py:114-124).  ``seq_parts`` is the number of
-    sequence segments for ``b200-seqpar``.
+    ``block_size`` is the reference's block (chunk) length.  Each device kernel walks the
+    sequence in chunks of a fixed length C (64 for the bf16 tensor-core kernel, 32 for the
+    3xTF32 and FFMA kernels): a block of ``block_size = k * C`` tokens is exactly k consecutive
+    kernel chunks -- the two-level block algebra is block-size invariant (reference
+    test_kernels.py:114-124) -- so any positive multiple of C is honoured, and ``run_method``
+    reports the opcount at C, the chunk actually used.  Other values raise UsageError.
+    ``row_block``/``col_block``/``term_size``/``mem_cap`` feed reference-only routes and are
+    accepted for signature parity.  ``seq_parts`` is the number of sequence segments for
+    ``b200-seqpar``.
     """
 
     block_size: int = 64
@@ -95,6 +99,24 @@ _COMPUTE = {
     MethodId.B200_RECURRENT: torch.float32,
     MethodId.B200_SEQPAR: torch.bfloat16,
 }
+
+
+def kernel_chunk(method: MethodId, inputs: AttnInputs) -> int:
+    """Token chunk of the kernel ``method`` runs for these inputs (1 for the row recurrence)."""
+    if method is MethodId.B200_RECURRENT:
+        return 1
+    cdt = _COMPUTE[method]
+    name = ops.prefill_kernel_name(inputs.rank, inputs.dim, cdt)
+    return {"prefill_tc": TC_CHUNK, "prefill_tf32": TF32_CHUNK}.get(name, SIMT_CHUNK)
+
+
+def _check_block_size(method: MethodId, params: "BlockParams", chunk: int) -> None:
+    bs = params.block_size
+    if method is MethodId.B200_RECURRENT or bs is None:
+        return
+    if not isinstance(bs, (int, np.integer)) or bs < 1 or bs % chunk:
+        raise UsageError(f"{method.value} runs chunks of {chunk} tokens for these inputs: block_size must "
+                         f"be a positive multiple of {chunk} (got {bs!r})")
 
 
 def _to_device(x, dtype):
@@ -285,6 +307,8 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
     if validate:
         validate_inputs(inputs)
     cdt = _COMPUTE[method]
+    chunk = kernel_chunk(method, inputs)
+    _check_block_size(method, params, chunk)
     host = not inputs.on_device
     torch_host = inputs.on_device and not inputs.v.is_cuda
     in_dtype = inputs.v.dtype
@@ -305,7 +329,6 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
             kernel = "auto"
             split = max(1, int(params.seq_parts)) if method is MethodId.B200_SEQPAR else None
             run = lambda q, k, v, l2, o: ops.prefill(q, k, v, l2, out=o, kernel=kernel, seq_split=split)  # noqa: E731
-            chunk = SIMT_CHUNK if method is MethodId.B200_CHUNKED_F32 else TC_CHUNK
             ops_count = ops.chunked_opcount(inputs.batch, inputs.heads, inputs.seqlen, inputs.rank,
                                             inputs.dim, inputs.decay, chunk)
         # the row recurrence is one serial chain per (b, h): few, wide pieces keep the SMs busy
@@ -315,18 +338,12 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
     k = _to_device(inputs.c, cdt)
     v = _to_device(inputs.v, cdt)
     log2g = ops.log2_gamma(inputs.gamma, inputs.decay, device=q.device)
-    if method is MethodId.B200_CHUNKED:
+    if method in (MethodId.B200_CHUNKED, MethodId.B200_CHUNKED_F32):
         out_dev = ops.prefill(q, k, v, log2g, kernel="auto")
-        chunk = TC_CHUNK
-    elif method is MethodId.B200_CHUNKED_F32:
-        out_dev = ops.prefill(q, k, v, log2g, kernel="auto")
-        chunk = SIMT_CHUNK
     elif method is MethodId.B200_SEQPAR:
         out_dev = _seqpar(q, k, v, log2g, max(1, int(params.seq_parts)), "auto")
-        chunk = TC_CHUNK
     else:
         out_dev = _recurrent(q, k, v, log2g)
-        chunk = 1
     ops_count = ops.chunked_opcount(inputs.batch, inputs.heads, inputs.seqlen, inputs.rank,
                                     inputs.dim, inputs.decay, chunk)
     if method is MethodId.B200_RECURRENT:

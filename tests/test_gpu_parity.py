@@ -570,3 +570,42 @@ def test_decode_fuzz(la, seed):
     got = torch.stack(outs, 2).cpu().numpy()
     assert orc.max_rel_error(got, ref) <= TOL_F32, (B, H, dk, dv)
     assert orc.max_rel_error(st.cpu().numpy(), ref_s) <= TOL_F32, (B, H, dk, dv)
+
+
+def test_block_size_honoured_or_rejected(la, golden):
+    """BlockParams.block_size (reference kernels.py:47-61): a block of k kernel chunks is k chunks,
+    so every positive multiple of the kernel chunk gives the same output (block-size invariance,
+    reference test_kernels.py:114-124) with the opcount at the chunk actually used; any other
+    value raises UsageError instead of being ignored."""
+    from paper_2501_02573_b200 import ops
+    from paper_2501_02573_b200.kernels import kernel_chunk
+    b, c, v = orc.gen_inputs(2, 3, 333, 64, 64, np.float32, 12)
+    gam = [0.0, 0.9, 1.0]
+    ref = orc.oracle_attn(orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v), gam, True)
+    dev_in = la.make_inputs(*(dev(orc.bf16_round(x), torch.bfloat16) for x in (b, c, v)), gamma=gam, decay=True)
+    assert kernel_chunk(la.MethodId.B200_CHUNKED, dev_in) == 64
+    outs = {}
+    for bs in (64, 128, 256):
+        out, opc = la.run_method(la.MethodId.B200_CHUNKED, dev_in, la.BlockParams(block_size=bs))
+        outs[bs] = out
+        assert opc == ops.chunked_opcount(2, 3, 333, 64, 64, True, 64)
+        assert orc.max_rel_error(out.float().cpu().numpy(), ref) <= TOL_BF16
+    assert torch.equal(outs[64], outs[128]) and torch.equal(outs[64], outs[256])
+    for bad in (1, 32, 48, 0, -64):
+        with pytest.raises(la.UsageError):
+            la.run_method(la.MethodId.B200_CHUNKED, dev_in, la.BlockParams(block_size=bad))
+    f32_in = la.make_inputs(b, c, v, gam, True)                 # host f32: 3xTF32 kernel, chunk 32
+    assert kernel_chunk(la.MethodId.B200_CHUNKED_F32, f32_in) == 32
+    ref32 = orc.oracle_attn(b, c, v, gam, True)
+    prev = None
+    for bs in (32, 64, 128):
+        out, opc = la.run_method(la.MethodId.B200_CHUNKED_F32, f32_in, la.BlockParams(block_size=bs))
+        assert opc == ops.chunked_opcount(2, 3, 333, 64, 64, True, 32)
+        assert orc.max_rel_error(out, ref32) <= TOL_F32
+        if prev is not None:
+            np.testing.assert_array_equal(out, prev)
+        prev = out
+    with pytest.raises(la.UsageError):
+        la.run_method(la.MethodId.B200_CHUNKED_F32, f32_in, la.BlockParams(block_size=16))
+    # the row recurrence has no chunk: any block size is accepted
+    la.run_method(la.MethodId.B200_RECURRENT, f32_in, la.BlockParams(block_size=7))
