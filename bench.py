@@ -608,6 +608,22 @@ def run_ours(args):
                   "api": f"run_method({meth.value}) on pageable numpy f32 arrays (pinned staging inside)"}
         del npin, inputs
 
+    # the public front door on device tensors: la.decode(la.make_inputs(q, k, v, ...)) per step
+    # (shape/gamma validation, the deferred NaN/Inf check, auto dispatch, one prefill), host wall
+    # clock with a device synchronisation per step, against the bare kernel's device time
+    front = None
+    if not args.no_extra:
+        la.decode(la.make_inputs(q, k, v, gamma=gam, decay=True))
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(10):
+            la.decode(la.make_inputs(q, k, v, gamma=gam, decay=True))
+        torch.cuda.synchronize()
+        fd_ms = max_over_ranks((time.perf_counter() - t0) / 10 * 1e3)
+        front = {"api": "la.decode(la.make_inputs(q, k, v, gamma, decay=True)) on configs[1] CUDA bf16 tensors",
+                 "ms_per_call": fd_ms, "bare_kernel_ms": ms, "ratio_to_bare_kernel": fd_ms / ms}
+
     # decode step (configs[3]): 1024 single-token steps, state 256x32x128x128 fp32 (512 MiB)
     dec = None
     if not args.no_decode:
@@ -645,6 +661,7 @@ def run_ours(args):
                 "ms_per_step": e2e_s * 1e3,
                 "api": "run_method(b200-chunked) on pinned host bf16 tensors (H2D | kernel | D2H overlapped per batch piece)"},
         "e2e_numpy_f32": e2e_np,
+        "front_door": front,
         "gpu_launches": int(max_over_ranks(launches)),
         "clocks": clk.summary(),
         "decode": dec,

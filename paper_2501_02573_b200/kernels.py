@@ -36,7 +36,7 @@ import torch
 
 from . import ops
 from .errors import LinAttnError, UsageError
-from .tensor import AttnInputs, validate_inputs
+from .tensor import DEFER, AttnInputs, check_output_then_inputs, validate_inputs
 
 DEFAULT_MEM_CAP = 2 << 30  # kept for signature parity with the reference (oracle.py:16)
 TC_CHUNK = 64      # token chunk of the bf16 tensor-core kernel (the reference default, kernels.py:57)
@@ -305,7 +305,7 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
     if params is None:
         params = BlockParams()
     if validate:
-        validate_inputs(inputs)
+        validate_inputs(inputs, check_values=DEFER)   # CUDA inputs: checked through the output below
     cdt = _COMPUTE[method]
     chunk = kernel_chunk(method, inputs)
     _check_block_size(method, params, chunk)
@@ -344,6 +344,8 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
         out_dev = _seqpar(q, k, v, log2g, max(1, int(params.seq_parts)), "auto")
     else:
         out_dev = _recurrent(q, k, v, log2g)
+    if validate:
+        check_output_then_inputs(inputs, out_dev)
     ops_count = ops.chunked_opcount(inputs.batch, inputs.heads, inputs.seqlen, inputs.rank,
                                     inputs.dim, inputs.decay, chunk)
     if method is MethodId.B200_RECURRENT:

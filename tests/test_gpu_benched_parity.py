@@ -171,6 +171,9 @@ def test_ops_reject_mismatched_shapes(ops):
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
 def test_device_finiteness_scan(ops, dt):
+    """validate_inputs on CUDA tensors: one fused scan names the first non-finite flat index like
+    the reference check_finite (tensor.py:20-25), incl. 16-byte unaligned views; decode on the
+    same inputs raises the same DataError through its deferred (output-first) check."""
     import paper_2501_02573_b200 as la
     from paper_2501_02573_b200.errors import DataError
     n = 1 << 20
@@ -178,18 +181,45 @@ def test_device_finiteness_scan(ops, dt):
         base = [torch.randn(n + offset, device="cuda").to(dt) for _ in range(3)]
         views = [x[offset:].view(1, 1, n // 64, 64) for x in base]   # offset: 16-byte unaligned views
         views[which].view(-1)[idx] = float("inf") if idx % 2 else float("nan")
+        inp = la.make_inputs(*views, gamma=0.9, decay=True)
         with pytest.raises(DataError, match=f"{name} has a non-finite entry at flat index {idx}$"):
-            la.make_inputs(*views, gamma=0.9, decay=True)
+            la.validate_inputs(inp)
+        inp = la.make_inputs(*views, gamma=0.9, decay=True)
+        with pytest.raises(DataError, match=f"{name} has a non-finite entry at flat index {idx}$"):
+            la.decode(inp)
     # first offending tensor in B, C, V order, smallest index within it
     xs = [torch.randn(4, 2, 50, 16, device="cuda").to(dt) for _ in range(3)]
     xs[2].view(-1)[3] = float("nan")
     xs[1].view(-1)[900] = float("nan")
     xs[1].view(-1)[77] = float("inf")
     with pytest.raises(DataError, match="C has a non-finite entry at flat index 77$"):
-        la.make_inputs(*xs, gamma=0.5, decay=True)
+        la.decode(la.make_inputs(*xs, gamma=0.5, decay=True))
+
+
+@pytest.mark.parametrize("gamma", [0.0, 0.5, 1.0])
+@pytest.mark.parametrize("which", [0, 1, 2])
+def test_nonfinite_input_always_reaches_the_output(ops, gamma, which):
+    """The deferred check relies on every NaN/Inf input element reaching some output (a masked
+    product is NaN, not 0): one bad element anywhere, each method, gamma in {0, 0.5, 1}."""
+    import paper_2501_02573_b200 as la
+    from paper_2501_02573_b200.errors import DataError
+    rng = np.random.default_rng(which)
+    for method, dt, (dk, dv) in [("b200-chunked", torch.bfloat16, (128, 128)), ("b200-chunked", torch.bfloat16, (256, 512)),
+                                 ("b200-chunked", torch.bfloat16, (24, 40)), ("b200-chunked-f32", torch.float32, (64, 64)),
+                                 ("b200-chunked-f32", torch.float32, (6, 10)), ("b200-recurrent", torch.float32, (64, 64)),
+                                 ("b200-seqpar", torch.bfloat16, (128, 128))]:
+        N = 300
+        xs = [torch.randn(2, 3, N, d, device="cuda").to(dt) for d in (dk, dk, dv)]
+        pos = int(rng.integers(0, xs[which].numel()))
+        xs[which].view(-1)[pos] = float("nan") if pos % 2 else float("-inf")
+        with pytest.raises(DataError, match=f"{'BCV'[which]} has a non-finite entry at flat index {pos}$"):
+            la.decode(la.make_inputs(*xs, gamma=gamma, decay=True), method=method)
 
 
 def test_validation_runs_once_until_modified(ops):
+    """make_inputs -> decode on CUDA tensors: no input scan at all when the output is finite (one
+    prefill + one output scan); the next decode of the same unmodified inputs only runs the
+    prefill; an in-place write makes the check run again."""
     import paper_2501_02573_b200 as la
     from paper_2501_02573_b200 import _lib
     from paper_2501_02573_b200.errors import DataError
@@ -197,10 +227,14 @@ def test_validation_runs_once_until_modified(ops):
     inp = la.make_inputs(*xs, gamma=0.9, decay=True)
     torch.cuda.synchronize()
     n0 = _lib.launch_count()
-    la.decode(inp)                                    # validated already: no rescan, one prefill
+    la.decode(inp)
     torch.cuda.synchronize()
-    assert _lib.launch_count() - n0 == 1
-    xs[1][0, 0, 5, 3] = float("nan")                  # in-place write bumps the tensor version
+    assert _lib.launch_count() - n0 == 2                   # prefill + output scan
+    n0 = _lib.launch_count()
+    la.decode(inp)
+    torch.cuda.synchronize()
+    assert _lib.launch_count() - n0 == 1                   # already established: prefill only
+    xs[1][0, 0, 5, 3] = float("nan")                       # in-place write bumps the tensor version
     with pytest.raises(DataError, match="C has a non-finite entry at flat index 323$"):
         la.decode(inp)
 
