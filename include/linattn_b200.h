@@ -160,6 +160,18 @@ LINATTN_API int linattn_recurrent(const void* q, const void* k, const void* v, v
 /* Kernel family LINATTN_KERNEL_AUTO resolves to for this shape/dtype (TC or SIMT). */
 LINATTN_API int linattn_prefill_kernel(int64_t dk, int64_t dv, int dtype);
 
+/* linattn_prefill plus the entry contract's NaN/Inf check on the way (reference check_finite,
+ * tensor.py:20-25): *nonfinite (DEVICE int64, caller-initialised to INT64_MAX) is lowered below
+ * INT64_MAX if the output holds a NaN/Inf.  Every non-finite input element reaches some output (a
+ * NaN/Inf times a zero mask weight is NaN), so a clean output proves clean inputs; the caller then
+ * scans the inputs (linattn_nonfinite_index) only to name the offending entry.  The bf16 tensor-core
+ * kernel checks its outputs in its epilogue (no extra memory traffic); other kernels are followed by
+ * one scan of the output. */
+LINATTN_API int linattn_prefill_checked(const void* q, const void* k, const void* v, void* o,
+                                        const float* log2g, const float* s_in, float* s_out,
+                                        int64_t B, int64_t H, int64_t N, int64_t dk, int64_t dv,
+                                        int dtype, int kernel, int64_t* nonfinite, void* stream);
+
 /* Finiteness scan of the entry contract (reference check_finite, tensor.py:20-25), one HBM pass:
  * atomically lowers *first_bad (DEVICE int64, initialised by the caller to INT64_MAX) to the
  * smallest flat index of a NaN/Inf among the n elements of x (dtype f32 or bf16).  Scanning q, k

@@ -41,6 +41,8 @@ _SIGS = {
     "linattn_segment_prefix": [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
     "linattn_state_at": [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
     "linattn_nonfinite_index": [_vp, _i64, ctypes.c_int, _vp, _vp],
+    "linattn_prefill_checked": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64,
+                                ctypes.c_int, ctypes.c_int, _vp, _vp],
     "linattn_release_workspace": [],
     "linattn_last_error": [],
     "linattn_abi_version": [],

@@ -16,6 +16,11 @@ namespace linattn {
 
 extern float* g_tf32_dump;
 static thread_local std::string g_last_error;
+static thread_local int64_t* g_nf_slot = nullptr;
+static thread_local bool g_nf_consumed = false;
+
+int64_t* nonfinite_slot() { return g_nf_slot; }
+void mark_nonfinite_consumed() { g_nf_consumed = true; }
 static thread_local int64_t g_launches = 0;
 
 void count_launch() { ++g_launches; }
@@ -484,6 +489,22 @@ int linattn_recurrent(const void* q, const void* k, const void* v, void* o, cons
                 "(got %lld, %lld)", (long long)dk, (long long)dv);
   return cuda_status(launch_recurrent(q, k, v, o, log2g, s_in, s_out, s, dtype, (cudaStream_t)stream),
                      "recurrent");
+}
+
+int linattn_prefill_checked(const void* q, const void* k, const void* v, void* o, const float* log2g,
+                            const float* s_in, float* s_out, int64_t B, int64_t H, int64_t N, int64_t dk,
+                            int64_t dv, int dtype, int kernel, int64_t* nonfinite, void* stream) {
+  if (!nonfinite) return fail(LINATTN_EPARAM, "null nonfinite slot");
+  g_nf_slot = nonfinite;
+  g_nf_consumed = false;
+  int st = linattn_prefill(q, k, v, o, log2g, s_in, s_out, B, H, N, dk, dv, dtype, kernel, stream);
+  const bool fused = g_nf_consumed;
+  g_nf_slot = nullptr;
+  g_nf_consumed = false;
+  if (st != LINATTN_OK || fused) return st;
+  // this shape ran a kernel without the fused check: one scan of the output instead
+  return cuda_status(launch_nonfinite(o, B * H * N * dv, dtype, nonfinite, (cudaStream_t)stream),
+                     "nonfinite_index (prefill output)");
 }
 
 int linattn_nonfinite_index(const void* x, int64_t n, int dtype, int64_t* first_bad, void* stream) {

@@ -241,4 +241,10 @@ cudaError_t launch_nonfinite(const void* x, int64_t n, int dtype, int64_t* first
 
 void count_launch();
 
+// Fused entry-contract check (linattn_prefill_checked): a thread-local device int64 slot that a
+// full prefill launch lowers to 0 when it writes a non-finite output (kernels that fuse the check
+// mark it consumed; for the others the C side scans the output into the slot afterwards).
+int64_t* nonfinite_slot();
+void mark_nonfinite_consumed();
+
 }  // namespace linattn

@@ -94,7 +94,8 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                        const float* __restrict__ log2g, const float* __restrict__ s_in,
                        float* __restrict__ s_out, int H, int N, int dv, int state_only,
-                       const SegArgs sa, const Balance bal, unsigned long long* __restrict__ trace) {
+                       const SegArgs sa, const Balance bal, unsigned long long* __restrict__ trace,
+                       unsigned long long* __restrict__ nonfinite) {
   using G = Cfg<DK, STAGES, SO>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -329,6 +330,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     // stmatrix row address of this thread: matrix m = lane/8 of each x4 group, row lane%8
     const int mrow = lane & 7;
     const int mi = lane >> 3;                  // 0: (d0, t), 1: (d0+8, t), 2: (d0, t+8), 3: (d0+8, t+8)
+    uint32_t out_bad = 0;                      // any non-finite output value seen (fused entry check)
     const int md = d0 + (mi & 1) * 8;          // 8-aligned dv row of the tile this address serves
     int gc = 0;
     for (int it = 0; it < nitems; ++it) {
@@ -441,6 +443,10 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
             pk[2 * r + 1] = pack_bf16x2(fmaf(w0, __uint_as_float(rx[4 * r + 2]), __uint_as_float(ro[4 * r + 2])),
                                         fmaf(w1, __uint_as_float(rx[4 * r + 3]), __uint_as_float(ro[4 * r + 3])));
           }
+          // entry-contract NaN/Inf check fused into the epilogue: every non-finite input reaches
+          // some output, so a clean output proves clean inputs (bf16 exponent all ones)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) out_bad |= __vcmpeq2(pk[i] & 0x7f807f80u, 0x7f807f80u);
 #pragma unroll
           for (int rr = 0; rr < 4; rr += 2) {      // two 8-token groups per stmatrix.x4
             const int tt = q4 * 32 + rr * 8 + (mi >> 1) * 8 + mrow;     // token row this lane addresses
@@ -460,6 +466,7 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       }
       LA_WRITE_STATE();
     }
+    if (nonfinite != nullptr && __any_sync(0xffffffffu, out_bad != 0u) && lane == 0) atomicMin(nonfinite, 0ull);
     if (leader) bulk_wait<0>();
   } else {
     if (warp == 12) {
@@ -1271,13 +1278,16 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   if (err != cudaSuccess) return err;
   const dim3 grid = bal.on ? dim3((unsigned)ctas)
                            : dim3((unsigned)((s.dv + kDVT - 1) / kDVT), (unsigned)BH, (unsigned)nz);
+  // fused NaN/Inf output check (linattn_prefill_checked): full launches only
+  unsigned long long* nf = state_only ? nullptr : reinterpret_cast<unsigned long long*>(nonfinite_slot());
+  if (nf) mark_nonfinite_consumed();
   if (bal.on) {   // the balanced launch follows the memset of its flags: plain stream order
     kern<<<grid, v2::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out,
                                                   (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
-                                                  sa, bal, g_trace);
+                                                  sa, bal, g_trace, nf);
   } else {
     err = launch_pdl(kern, grid, dim3(v2::kThreads), G::SMEM, stream, mq, mk, mv, mo, log2g, s_in, s_out,
-                     (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0, sa, bal, g_trace);
+                     (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0, sa, bal, g_trace, nf);
     if (err != cudaSuccess) return err;
   }
   count_launch();

@@ -36,7 +36,8 @@ import torch
 
 from . import ops
 from .errors import LinAttnError, UsageError
-from .tensor import DEFER, AttnInputs, check_output_then_inputs, validate_inputs
+from .tensor import (DEFER, AttnInputs, check_finite_all, check_output_then_inputs, finite_check_pending,
+                     mark_finite, validate_inputs)
 
 DEFAULT_MEM_CAP = 2 << 30  # kept for signature parity with the reference (oracle.py:16)
 TC_CHUNK = 64      # token chunk of the bf16 tensor-core kernel (the reference default, kernels.py:57)
@@ -99,6 +100,22 @@ _COMPUTE = {
     MethodId.B200_RECURRENT: torch.float32,
     MethodId.B200_SEQPAR: torch.bfloat16,
 }
+
+
+_INT64_MAX = (1 << 63) - 1
+_NF_SLOTS = threading.local()
+
+
+def _nonfinite_slot(device) -> torch.Tensor:
+    """A per-thread, per-device int64 verdict slot reset to INT64_MAX on the current stream."""
+    slots = getattr(_NF_SLOTS, "d", None)
+    if slots is None:
+        slots = _NF_SLOTS.d = {}
+    slot = slots.get(device)
+    if slot is None:
+        slot = slots[device] = torch.empty(1, dtype=torch.int64, device=device)
+    slot.fill_(_INT64_MAX)
+    return slot
 
 
 def kernel_chunk(method: MethodId, inputs: AttnInputs) -> int:
@@ -337,8 +354,17 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
     q = _to_device(inputs.b, cdt)
     k = _to_device(inputs.c, cdt)
     v = _to_device(inputs.v, cdt)
-    log2g = ops.log2_gamma(inputs.gamma, inputs.decay, device=q.device)
-    if method in (MethodId.B200_CHUNKED, MethodId.B200_CHUNKED_F32):
+    log2g = ops.log2_gamma_cached(inputs.gamma, inputs.decay, q.device)
+    fused_check = validate and finite_check_pending(inputs) and method is not MethodId.B200_RECURRENT
+    if method in (MethodId.B200_CHUNKED, MethodId.B200_CHUNKED_F32) and fused_check:
+        # the entry contract's NaN/Inf check rides on the launch (fused into the bf16 tensor-core
+        # epilogue); the inputs are rescanned only if the output is not clean
+        slot = _nonfinite_slot(q.device)
+        out_dev = ops.prefill(q, k, v, log2g, kernel="auto", nonfinite=slot)
+        if int(slot.item()) != _INT64_MAX:
+            check_finite_all((("B", inputs.b), ("C", inputs.c), ("V", inputs.v)))
+        mark_finite(inputs)
+    elif method in (MethodId.B200_CHUNKED, MethodId.B200_CHUNKED_F32):
         out_dev = ops.prefill(q, k, v, log2g, kernel="auto")
     elif method is MethodId.B200_SEQPAR:
         out_dev = _seqpar(q, k, v, log2g, max(1, int(params.seq_parts)), "auto")

@@ -121,6 +121,24 @@ def log2_gamma(gammas, decay: bool = True, device=None) -> torch.Tensor:
     return t.to(device) if device is not None else t
 
 
+_L2G_CACHE: dict = {}
+
+
+def log2_gamma_cached(gammas, decay: bool, device) -> torch.Tensor:
+    """log2_gamma on ``device``, cached per (gammas, decay, device) for the library's own calls
+    (saves a pageable host-to-device copy per call); callers must not modify the result."""
+    dev = torch.device(device)
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    key = (tuple(float(g) for g in gammas), bool(decay), dev)
+    t = _L2G_CACHE.get(key)
+    if t is None:
+        if len(_L2G_CACHE) > 256:
+            _L2G_CACHE.clear()
+        t = _L2G_CACHE[key] = log2_gamma(gammas, decay, dev)
+    return t
+
+
 _MAX_GRID_Y = 65535   # the sequence kernels put batch*heads on grid.y
 
 
@@ -134,13 +152,20 @@ def _batch_chunks(B: int, H: int):
 
 @_on_tensor_device
 def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "auto",
-            seq_split: int | None = None):
+            seq_split: int | None = None, nonfinite=None):
     """O = (Q K^T (.) M_gamma) V on device; optional initial/end state (fp32).
 
     ``seq_split``: None lets the library split the sequence across SMs when batch x head
     leaves them idle (``seq_plan``); 1 forces a single pass; P > 1 forces P segments
     (two-phase: segment-local state pass, then every segment seeded in parallel).
+    ``nonfinite``: optional int64 [1] CUDA tensor holding INT64_MAX; lowered if the output holds a
+    NaN/Inf (fused into the bf16 tensor-core kernel's epilogue, else one scan of the output).
     """
+    if nonfinite is not None and seq_split is not None:
+        out = prefill(q, k, v, log2g, s_in=s_in, s_out=s_out, out=out, kernel=kernel, seq_split=seq_split)
+        _lib.check(_lib.load().linattn_nonfinite_index(out.data_ptr(), out.numel(), _dtype_code(out),
+                                                      nonfinite.data_ptr(), _stream()))
+        return out
     if seq_split is not None and seq_split > 1:
         n = q.shape[2]
         seg = -(-n // seq_split)
@@ -168,9 +193,13 @@ def prefill(q, k, v, log2g, *, s_in=None, s_out=None, out=None, kernel: str = "a
     lib = _lib.load()
     for b0, b1 in _batch_chunks(B, H):   # more than 65535 (batch, head) units: one launch per chunk
         sl = (lambda t: None if t is None else t[b0:b1])   # noqa: E731
-        _lib.check(lib.linattn_prefill(q[b0:b1].data_ptr(), k[b0:b1].data_ptr(), v[b0:b1].data_ptr(),
-                                       out[b0:b1].data_ptr(), log2g.data_ptr(), _ptr(sl(s_in)), _ptr(sl(s_out)),
-                                       b1 - b0, H, N, dk, dv, _dtype_code(q), _KERNELS[kernel], _stream()))
+        args = (q[b0:b1].data_ptr(), k[b0:b1].data_ptr(), v[b0:b1].data_ptr(), out[b0:b1].data_ptr(),
+                log2g.data_ptr(), _ptr(sl(s_in)), _ptr(sl(s_out)), b1 - b0, H, N, dk, dv, _dtype_code(q),
+                _KERNELS[kernel])
+        if nonfinite is None:
+            _lib.check(lib.linattn_prefill(*args, _stream()))
+        else:
+            _lib.check(lib.linattn_prefill_checked(*args, nonfinite.data_ptr(), _stream()))
     return out
 
 

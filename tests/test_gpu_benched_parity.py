@@ -217,9 +217,10 @@ def test_nonfinite_input_always_reaches_the_output(ops, gamma, which):
 
 
 def test_validation_runs_once_until_modified(ops):
-    """make_inputs -> decode on CUDA tensors: no input scan at all when the output is finite (one
-    prefill + one output scan); the next decode of the same unmodified inputs only runs the
-    prefill; an in-place write makes the check run again."""
+    """make_inputs -> decode on CUDA tensors: no input scan at all when the output is finite (the
+    bf16 tensor-core prefill checks its outputs in its epilogue: one launch; other kernels add one
+    output scan); the next decode of the same unmodified inputs only runs the prefill; an
+    in-place write makes the check run again."""
     import paper_2501_02573_b200 as la
     from paper_2501_02573_b200 import _lib
     from paper_2501_02573_b200.errors import DataError
@@ -229,7 +230,12 @@ def test_validation_runs_once_until_modified(ops):
     n0 = _lib.launch_count()
     la.decode(inp)
     torch.cuda.synchronize()
-    assert _lib.launch_count() - n0 == 2                   # prefill + output scan
+    assert _lib.launch_count() - n0 == 1                   # prefill with the fused output check
+    f32 = la.make_inputs(*(x.float() for x in xs), gamma=0.9, decay=True)
+    n0 = _lib.launch_count()
+    la.decode(f32)
+    torch.cuda.synchronize()
+    assert _lib.launch_count() - n0 == 2                   # 3xTF32 prefill + one output scan
     n0 = _lib.launch_count()
     la.decode(inp)
     torch.cuda.synchronize()
