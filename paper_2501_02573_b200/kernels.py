@@ -112,9 +112,8 @@ def _nonfinite_slot(device) -> torch.Tensor:
     if slots is None:
         slots = _NF_SLOTS.d = {}
     slot = slots.get(device)
-    if slot is None:
-        slot = slots[device] = torch.empty(1, dtype=torch.int64, device=device)
-    slot.fill_(_INT64_MAX)
+    if slot is None:   # a clean verdict leaves the slot at INT64_MAX: it is reset only after a hit
+        slot = slots[device] = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=device)
     return slot
 
 
@@ -362,6 +361,7 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
         slot = _nonfinite_slot(q.device)
         out_dev = ops.prefill(q, k, v, log2g, kernel="auto", nonfinite=slot)
         if int(slot.item()) != _INT64_MAX:
+            slot.fill_(_INT64_MAX)
             check_finite_all((("B", inputs.b), ("C", inputs.c), ("V", inputs.v)))
         mark_finite(inputs)
     elif method in (MethodId.B200_CHUNKED, MethodId.B200_CHUNKED_F32):
