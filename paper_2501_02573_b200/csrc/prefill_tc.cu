@@ -23,6 +23,10 @@
 #include "common.cuh"
 #include "sm100.cuh"
 
+#ifndef TC_SMEM_SPACE
+#define TC_SMEM_SPACE 1
+#endif
+
 namespace linattn {
 namespace {
 
@@ -97,8 +101,13 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                        const SegArgs sa, const Balance bal, unsigned long long* __restrict__ trace,
                        unsigned long long* __restrict__ nonfinite) {
   using G = Cfg<DK, STAGES, SO>;
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+#if TC_SMEM_SPACE
+  // aligned by pointer arithmetic so ptxas keeps the shared address space (LDS/STS, not generic)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+#else
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+#endif
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   uint64_t* empty = full + STAGES;
   uint64_t* mma1_bar = empty + STAGES;   // P^T accumulator ready (single buffer)
@@ -695,8 +704,13 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
   static_assert(G::KB % MC == 0, "Q/K boxes split evenly over the cluster");
   constexpr uint16_t kMask = (uint16_t)((1u << MC) - 1);
   constexpr int SCOL = DK / 2;                     // state columns per state warp
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+#if TC_SMEM_SPACE
+  // aligned by pointer arithmetic so ptxas keeps the shared address space (LDS/STS, not generic)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+#else
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+#endif
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);   // Q/K ring
   uint64_t* empty = full + STAGES;
   uint64_t* vfull = empty + STAGES;        // [VST] V ring
