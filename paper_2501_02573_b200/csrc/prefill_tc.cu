@@ -23,6 +23,12 @@
 #include "common.cuh"
 #include "sm100.cuh"
 
+#ifndef V3_PUB_ILP
+#define V3_PUB_ILP 0
+#endif
+#ifndef V3_PACK_ALU
+#define V3_PACK_ALU 0
+#endif
 #ifndef TC_SMEM_SPACE
 #define TC_SMEM_SPACE 1
 #endif
@@ -662,6 +668,20 @@ __device__ __forceinline__ void scale_row_blocks(const uint8_t* src, uint8_t* ds
 
 __device__ __forceinline__ uint32_t dup_lo(uint32_t w2) { return (w2 & 0xFFFFu) | (w2 << 16); }
 
+// fp32 pair -> bf16x2 (round to nearest even) for the state publish: F2FP (cvt.rn.bf16x2.f32), or
+// with V3_PACK_ALU the same rounding on the integer pipes (F2FP showed as 14% of the issued
+// instructions of this kernel)
+__device__ __forceinline__ uint32_t pack_bf16x2_pub(float lo, float hi) {
+#if V3_PACK_ALU
+  uint32_t a = __float_as_uint(lo), b = __float_as_uint(hi);
+  a += 0x7fffu + ((a >> 16) & 1u);
+  b += 0x7fffu + ((b >> 16) & 1u);
+  return __byte_perm(a, b, 0x7632);
+#else
+  return pack_bf16x2(lo, hi);
+#endif
+}
+
 // Lazy decay normalisation.  gamma is a per-head SCALAR, so the state is kept as S_c = sig_c T_c:
 // the update S_{c+1} = gamma^L S_c + V'^T K becomes T_{c+1} = T_c + (V'/sig_{c+1})^T K with
 // sig_{c+1} = sig_c gamma^L -- the 1/sig factor rides on V' (16 KiB, already rescaled every
@@ -1060,6 +1080,33 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       lz.step(pwv[L]);
       // publish bf16 T_c for O_inter(c); rewrite T only when renormalising (T <- sig gamma^L T)
       if (!state_only || lz.renorm) {
+#if V3_PUB_ILP
+        // two 32-column TMEM loads in flight per wait: the publish is on the per-chunk chain
+#pragma unroll 1
+        for (int cb = 0; cb < SCOL / 32; cb += 2) {
+          float sv[32], sw[32];
+          tmem_ld32(ta_s + cb * 32, sv);
+          tmem_ld32(ta_s + (cb + 1) * 32, sw);
+          tmem_wait_ld();
+          if (!state_only) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2_pub(sv[2 * i], sv[2 * i + 1]);
+            tmem_st16(ta_sb + cb * 16, pk);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2_pub(sw[2 * i], sw[2 * i + 1]);
+            tmem_st16(ta_sb + (cb + 1) * 16, pk);
+          }
+          if (lz.renorm) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sv[i] *= lz.rescale;
+            tmem_st32(ta_s + cb * 32, sv);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sw[i] *= lz.rescale;
+            tmem_st32(ta_s + (cb + 1) * 32, sw);
+          }
+        }
+#else
 #pragma unroll 1
         for (int cb = 0; cb < SCOL / 32; ++cb) {
           float sv[32];
@@ -1068,7 +1115,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
           if (!state_only) {
             uint32_t pk[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(sv[2 * i], sv[2 * i + 1]);
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2_pub(sv[2 * i], sv[2 * i + 1]);
             tmem_st16(ta_sb + cb * 16, pk);
           }
           if (lz.renorm) {
@@ -1077,6 +1124,7 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
             tmem_st32(ta_s + cb * 32, sv);
           }
         }
+#endif
         tmem_wait_st();
       }
       tc_fence_before();
