@@ -17,6 +17,9 @@ full cfg5_statepass prefill_tc_pipe 4 PROF_SHAPE=1,32,131072,128
 full cfg5_prefill prefill_tc_pipe 5 PROF_SHAPE=1,32,131072,128
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:simt -s 1 -c 1 \
     -o $OUT/prof_fp32_prefill_$TAG python tools/f32_once.py > $OUT/prof_fp32_prefill_$TAG.log 2>&1
+PROF_DTYPE=f32 PROF_KERNEL=tf32 PROF_SHAPE=8,32,8192,128 timeout 600 ncu --set full --clock-control none \
+    --import-source on -k regex:prefill_tf32 -s 2 -c 1 -o $OUT/prof_tf32_prefill_$TAG python tools/prof_driver.py \
+    > $OUT/prof_tf32_prefill_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_step -s 5 -c 1 \
     -o $OUT/prof_decode_$TAG python bench.py --steps 1 --warmup 3 --no-cpu --no-extra --decode-steps 64 \
     > $OUT/prof_decode_$TAG.log 2>&1

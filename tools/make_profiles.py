@@ -22,12 +22,16 @@ CAPTURES = [
     ("cfg5_prefill", "prefill_split", 32 * 131072 * 1024, "configs[4] phase B: 4 seeded segments x 32 heads"),
     ("decode", "decode_step", 256 * 32 * 132096, "configs[3] decode step B=256,H=32,d=128"),
     ("fp32_prefill", "prefill_simt_fp32", 8 * 32 * 2048 * 2048,
-     "fp32 parity mode (FFMA) B=8,H=32,N=2048,d=128 (tools/f32_once.py): balanced, cp.async staging"),
+     "fp32 FFMA kernel B=8,H=32,N=2048,d=128 (tools/f32_once.py): balanced, cp.async staging"),
+    ("tf32_prefill", "prefill_tf32", 8 * 32 * 8192 * 2048,
+     "fp32 parity mode on the tensor cores (3xTF32) at the configs[1] shape B=8,H=32,N=8192,d=128"),
 ]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__block_size",
-           "launch__registers_per_thread", "lts__t_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
+           "launch__registers_per_thread", "lts__t_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]
 
 
 def raw_metrics(rep):
@@ -68,8 +72,9 @@ def launch_shares(path):
 def main(tag):
     gout = os.path.join(ROOT, "gpurun_out")
     prof = os.path.join(ROOT, "profiles")
+    rnd = tag[:2] if tag[:1] == "r" and tag[1:2].isdigit() else "r"
     summary = {"_source": f"ncu --set full --clock-control none, one launch per kernel (round tag {tag}); "
-                          "per-kernel summaries in profiles/r1_<name>_ncu.txt"}
+                          f"per-kernel summaries in profiles/{rnd}_<name>_ncu.txt"}
     import ncu_summary
     for name, key, alg, desc in CAPTURES:
         rep = os.path.join(gout, f"prof_{name}_{tag}.ncu-rep")
@@ -86,7 +91,11 @@ def main(tag):
                         "tensor_pipe_active_pct": m.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
                         "dram_throughput_pct": m.get("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
                         "grid": m.get("launch__grid_size"), "block": m.get("launch__block_size"),
-                        "registers": m.get("launch__registers_per_thread")}
+                        "registers": m.get("launch__registers_per_thread"),
+                        "smem_tc_wavefronts_pct": m.get(
+                            "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                        "smem_lsu_wavefronts_pct": m.get(
+                            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")}
         buf = io.StringIO()
         old = sys.stdout
         sys.stdout = buf
@@ -94,19 +103,19 @@ def main(tag):
             ncu_summary.main(rep, None, 30)
         finally:
             sys.stdout = old
-        with open(os.path.join(prof, f"r1_{name}_ncu.txt"), "w") as fh:
+        with open(os.path.join(prof, f"{rnd}_{name}_ncu.txt"), "w") as fh:
             fh.write(f"# {desc}\n# ncu --set full --clock-control none --import-source on (tools/gpu_profile.sh {tag})\n")
             fh.write(buf.getvalue())
     with open(os.path.join(prof, "ncu_summary.json"), "w") as fh:
         json.dump(summary, fh, indent=1)
     lpath = os.path.join(gout, f"launches_{tag}.csv")
     if os.path.exists(lpath):
-        with open(os.path.join(prof, "r1_launches_summary.txt"), "w") as fh:
+        with open(os.path.join(prof, f"{rnd}_launches_summary.txt"), "w") as fh:
             fh.write("ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 3 --warmup 3 "
                      "--no-cpu --decode-steps 64\n(cold-cache, serialised per-launch times; compare shares, not "
                      "absolutes)\n")
             fh.write("\n".join(launch_shares(lpath)) + "\n")
-        subprocess.run(["cp", lpath, os.path.join(prof, "r1_launches.csv")])
+        subprocess.run(["cp", lpath, os.path.join(prof, f"{rnd}_launches.csv")])
 
 
 if __name__ == "__main__":
