@@ -187,7 +187,7 @@ static int pick_family(const ShapeArgs& s, int dtype, int kernel, std::initializ
   const bool tf_ok = tf32_supported(s, dtype) && al;
   if (kernel == LINATTN_KERNEL_TC && !tc_ok)
     return fail(LINATTN_EUNSUPPORTED,
-                "tensor-core prefill needs bf16, dk in {64,128,256}, dv %% 64 == 0 and 16-byte aligned "
+                "tensor-core prefill needs bf16, dk <= 256, dk and dv multiples of 8 and 16-byte aligned "
                 "tensors (got dtype=%d dk=%lld dv=%lld)", dtype, (long long)s.dk, (long long)s.dv);
   if (kernel == LINATTN_KERNEL_TF32 && !tf_ok)
     return fail(LINATTN_EUNSUPPORTED,

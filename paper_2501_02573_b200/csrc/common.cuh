@@ -15,6 +15,12 @@ __device__ __forceinline__ float gpow(float log2g, float n) {
   return n == 0.f ? 1.f : exp2f(n * log2g);
 }
 
+// gamma^n for an integer count that may exceed 2^24 (exact in float only up to there): the
+// exponent n * log2(gamma) is formed in double before the float exp2.
+__device__ __forceinline__ float gpow_n(float log2g, long long n) {
+  return n == 0 ? 1.f : exp2f((float)((double)log2g * (double)n));
+}
+
 // Fast variant (ex2.approx) for the bf16 tensor-core path.
 __device__ __forceinline__ float gpow_fast(float log2g, float n) {
   float r;

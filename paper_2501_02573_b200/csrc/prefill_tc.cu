@@ -29,6 +29,9 @@
 #ifndef V3_PACK_ALU
 #define V3_PACK_ALU 0
 #endif
+#ifndef V3_PF_AHEAD
+#define V3_PF_AHEAD 2     // dk = 256: L2 prefetch distance (chunks) of the Q/K ring; 0 = off
+#endif
 #ifndef TC_SMEM_SPACE
 #define TC_SMEM_SPACE 1
 #endif
@@ -98,12 +101,12 @@ __device__ __forceinline__ uint32_t hmul2_bf16(uint32_t a, uint32_t b) {
 
 // BAL: balanced persistent work list (Balance); false = one unit per CTA from blockIdx, where
 // every item field is a compile-time-known function of blockIdx (no extra live registers).
-template <int DK, int STAGES, bool SO, bool BAL>
+template <int DK, int STAGES, bool SO, bool BAL, bool PADK>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                        const float* __restrict__ log2g, const float* __restrict__ s_in,
-                       float* __restrict__ s_out, int H, int N, int dv, int state_only,
+                       float* __restrict__ s_out, int H, int N, int dv, int dk_arg, int state_only,
                        const SegArgs sa, const Balance bal, unsigned long long* __restrict__ trace,
                        unsigned long long* __restrict__ nonfinite) {
   using G = Cfg<DK, STAGES, SO>;
@@ -138,7 +141,9 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
-  const size_t per_state = (size_t)gridDim.y * DK * dv;
+  // PADK: dk < DK (Q/K boxes past dk are TMA zero fill); external states are [BH][dkr][dv]
+  const int dkr = PADK ? dk_arg : DK;
+  const size_t per_state = (size_t)gridDim.y * dkr * dv;
 
   if (warp == 12 && lane == 0) {
     // balanced schedule: tickets in start order, so the range before ours is already running
@@ -372,13 +377,14 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         for (int j = 0; j < SC; j += 16) {
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            S[j + i] = (s_in && dv_ok) ? w_in * s_in[((size_t)w.bh * DK + col0 + j + i) * dv + jd] : 0.f;
+            S[j + i] = (s_in && dv_ok && (!PADK || col0 + j + i < dkr)) ? w_in * s_in[((size_t)w.bh * dkr + col0 + j + i) * dv + jd] : 0.f;
           for (int qi = 0; qi < sa.nloc; ++qi) {
             const float wq = seg_loc_weight(sa, qi, N, w.lo, lg);
             if (wq < 0.f || !dv_ok) continue;
-            const float* lq = sa.loc + qi * per_state + ((size_t)w.bh * DK + col0 + j) * dv + jd;
+            const float* lq = sa.loc + qi * per_state + ((size_t)w.bh * dkr + col0 + j) * dv + jd;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) S[j + i] = fmaf(wq, lq[(size_t)i * dv], S[j + i]);
+            for (int i = 0; i < 16; ++i)
+              if (!PADK || col0 + j + i < dkr) S[j + i] = fmaf(wq, lq[(size_t)i * dv], S[j + i]);
           }
         }
       }
@@ -393,10 +399,11 @@ prefill_tc_pipe_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       if (dv_ok) so = bal.hst + ((size_t)w.out_slot * DK + col0) * kDVT + d;                          \
       so_stride = kDVT;                                                                               \
     } else if (s_out && dv_ok && (BAL ? w.hi == N : (state_only || blockIdx.z == gridDim.z - 1))) { \
-      so = s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)w.bh * DK + col0) * dv + jd;  \
+      so = s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)w.bh * dkr + col0) * dv + jd; \
     }                                                                                                 \
-    if (so != nullptr) {                                                                              \
-      _Pragma("unroll") for (int i = 0; i < SC; ++i) so[(size_t)i * so_stride] = S[i];                \
+    if (so != nullptr) { /* hand-off slots hold all DK rows, external states the dkr real ones */    \
+      const int nrow = (!PADK || w.out_slot >= 0) ? SC : min(SC, dkr - col0);                         \
+      _Pragma("unroll") for (int i = 0; i < SC; ++i) if (i < nrow) so[(size_t)i * so_stride] = S[i];  \
     }                                                                                                 \
     if (w.out_slot >= 0) { /* release the hand-off to the next range's tail */                       \
       __threadfence();                                                                                \
@@ -712,12 +719,12 @@ struct Lazy {
 // BAL: balanced persistent schedule over cluster ranges (Balance mode 0: unit = (b*h, group of MC
 // dv tiles), tile = MC*128, hand-off slots per CTA = ticket*MC + cluster rank, gamma tables per
 // head in global memory because three roles read them across item boundaries).
-template <int DK, int STAGES, int MC, bool BAL>
+template <int DK, int STAGES, int MC, bool BAL, bool PADK>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                              const float* __restrict__ log2g, const float* __restrict__ s_in,
-                             float* __restrict__ s_out, int H, int N, int dv, int state_only,
+                             float* __restrict__ s_out, int H, int N, int dv, int dk_arg, int state_only,
                              const SegArgs sa, const Balance bal, unsigned long long* __restrict__ trace) {
   using G = Cfg<DK, STAGES>;
   static_assert(DK % 128 == 0 && kDVT == 128, "layout: two state warps per TMEM subpartition");
@@ -753,7 +760,9 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
-  const size_t per_state = (size_t)gridDim.y * DK * dv;
+  // PADK: dk < DK (Q/K boxes past dk are TMA zero fill); external states are [BH][dkr][dv]
+  const int dkr = PADK ? dk_arg : DK;
+  const size_t per_state = (size_t)gridDim.y * dkr * dv;
   int* wl = reinterpret_cast<int*>(tmem_slot + 2);   // BAL: ticket of this cluster's range
 
   if (warp == 2 && lane == 0) {
@@ -1018,11 +1027,13 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
     // write one local state per segment, full launches only the segment ending the sequence
     float* so = nullptr;
     size_t so_stride = dv;
+    int srows = dkr;                                     // hand-off slots hold all DK rows
     if (BAL && w.out_slot >= 0) {
       if (dv_ok) so = bal.hst + ((size_t)w.out_slot * DK + col0) * kDVT + d;
       so_stride = kDVT;
+      srows = DK;
     } else if (s_out && dv_ok && (BAL ? w.hi == N : (state_only || blockIdx.z == gridDim.z - 1))) {
-      so = s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)w.bh * DK + col0) * dv + jd;
+      so = s_out + (state_only ? blockIdx.z * per_state : 0) + ((size_t)w.bh * dkr + col0) * dv + jd;
     }
     if (it > 0) {
       // the previous item's last S update and O_inter are done before T is re-seeded
@@ -1047,19 +1058,22 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            sv[i] = (s_in && dv_ok) ? w_in * s_in[((size_t)w.bh * DK + col0 + cb * 32 + i) * dv + jd] : 0.f;
+            sv[i] = (s_in && dv_ok && (!PADK || col0 + cb * 32 + i < dkr))
+                        ? w_in * s_in[((size_t)w.bh * dkr + col0 + cb * 32 + i) * dv + jd] : 0.f;
           for (int qi = 0; qi < sa.nloc; ++qi) {
             const float wq = seg_loc_weight(sa, qi, N, w.lo, lg);
             if (wq < 0.f || !dv_ok) continue;
-            const float* lq = sa.loc + qi * per_state + ((size_t)w.bh * DK + col0 + cb * 32) * dv + jd;
+            const float* lq = sa.loc + qi * per_state + ((size_t)w.bh * dkr + col0 + cb * 32) * dv + jd;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) sv[i] = fmaf(wq, lq[(size_t)i * dv], sv[i]);
+            for (int i = 0; i < 32; ++i)
+              if (!PADK || col0 + cb * 32 + i < dkr) sv[i] = fmaf(wq, lq[(size_t)i * dv], sv[i]);
           }
         }
         if (nch == 0) {
           if (so) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * so_stride] = sv[i];
+            for (int i = 0; i < 32; ++i)
+              if (!PADK || col0 + cb * 32 + i < srows) so[(size_t)(cb * 32 + i) * so_stride] = sv[i];
           }
         } else {
           tmem_st32(ta_s + cb * 32, sv);
@@ -1131,15 +1145,20 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
       mbar_arrive(st_done);
       if (warp == 4) V3_TRACE(1, c);
     }
-    if (nch > 0 && so) {
+    // tcgen05.ld is warp-collective: the whole warp loads when any lane has a row to write (lanes
+    // past dv have none when dv is not a multiple of 32)
+    if (nch > 0 && __any_sync(0xffffffffu, so != nullptr)) {
       mbar_wait(mma_s_bar, (c - 1) & 1);
       tc_fence_after();
       for (int cb = 0; cb < SCOL / 32; ++cb) {
         float sv[32];
         tmem_ld32(ta_s + cb * 32, sv);
         tmem_wait_ld();
+        if (so) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) so[(size_t)(cb * 32 + i) * so_stride] = lz.sig * sv[i];   // S = sig T
+          for (int i = 0; i < 32; ++i)   // S = sig T
+            if (!PADK || col0 + cb * 32 + i < srows) so[(size_t)(cb * 32 + i) * so_stride] = lz.sig * sv[i];
+        }
       }
     }
     if (BAL && w.out_slot >= 0) {                 // release the hand-off to the next range's tail
@@ -1173,6 +1192,17 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
             tma_load_3d(st + G::Q_BYTES + kb * 8192, &tm_k, &full[s], kb * 64, t0, w.bh);
           }
         }
+        // The Q/K ring has only STAGES = 2 stages of 64 KiB (shared memory is full), so the load
+        // of chunk c + STAGES waits for chunk c's release; warm L2 with it now so that load
+        // is an L2 hit instead of a full HBM round trip on the per-chunk critical path.
+        if (V3_PF_AHEAD > 0 && t0 + V3_PF_AHEAD * kC < w.hi) {
+#pragma unroll
+          for (int j = 0; j < G::KB / MC; ++j) {
+            const int kb = (int)crank * (G::KB / MC) + j;
+            if (!state_only) tma_prefetch_l2_3d(&tm_q, kb * 64, t0 + V3_PF_AHEAD * kC, w.bh);
+            tma_prefetch_l2_3d(&tm_k, kb * 64, t0 + V3_PF_AHEAD * kC, w.bh);
+          }
+        }
        }
       }
       if constexpr (MC > 1) {   // peers' final releases have landed before this CTA may exit
@@ -1192,6 +1222,10 @@ prefill_tc_tmem_state_kernel(const __grid_constant__ CUtensorMap tm_q, const __g
 #pragma unroll
         for (int nb = 0; nb < kDVT / 64; ++nb)
           tma_load_3d(st + nb * 8192, &tm_v, &vfull[s], w.j0 + nb * 64, t0, w.bh);
+        if (V3_PF_AHEAD > 0 && t0 + VST * kC < w.hi) {
+#pragma unroll
+          for (int nb = 0; nb < kDVT / 64; ++nb) tma_prefetch_l2_3d(&tm_v, w.j0 + nb * 64, t0 + VST * kC, w.bh);
+        }
        }
       }
     }
@@ -1335,7 +1369,12 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   }
   CUtensorMap mo = mk;
   if (!state_only && !make_map(&mo, o, s.dv, s.N, BH)) return cudaErrorInvalidValue;
-  auto kern = bal.on ? v2::prefill_tc_pipe_kernel<DK, STAGES, SO, true> : v2::prefill_tc_pipe_kernel<DK, STAGES, SO, false>;
+  // dk < DK: the padded instantiation (the benched dk == DK kernels stay free of the row guards)
+  const bool padk = s.dk != DK;
+  auto kern = bal.on ? (padk ? v2::prefill_tc_pipe_kernel<DK, STAGES, SO, true, true>
+                             : v2::prefill_tc_pipe_kernel<DK, STAGES, SO, true, false>)
+                     : (padk ? v2::prefill_tc_pipe_kernel<DK, STAGES, SO, false, true>
+                             : v2::prefill_tc_pipe_kernel<DK, STAGES, SO, false, false>);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
   const dim3 grid = bal.on ? dim3((unsigned)ctas)
@@ -1345,11 +1384,11 @@ cudaError_t launch_pipe(const void* q, const void* k, const void* v, void* o, co
   if (nf) mark_nonfinite_consumed();
   if (bal.on) {   // the balanced launch follows the memset of its flags: plain stream order
     kern<<<grid, v2::kThreads, G::SMEM, stream>>>(mq, mk, mv, mo, log2g, s_in, s_out,
-                                                  (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0,
+                                                  (int)s.H, (int)s.N, (int)s.dv, (int)s.dk, state_only ? 1 : 0,
                                                   sa, bal, g_trace, nf);
   } else {
     err = launch_pdl(kern, grid, dim3(v2::kThreads), G::SMEM, stream, mq, mk, mv, mo, log2g, s_in, s_out,
-                     (int)s.H, (int)s.N, (int)s.dv, state_only ? 1 : 0, sa, bal, g_trace, nf);
+                     (int)s.H, (int)s.N, (int)s.dv, (int)s.dk, state_only ? 1 : 0, sa, bal, g_trace, nf);
     if (err != cudaSuccess) return err;
   }
   count_launch();
@@ -1363,8 +1402,11 @@ cudaError_t launch_tmem_state_mc(const CUtensorMap& mq, const CUtensorMap& mk, c
                                  cudaStream_t stream, const Balance& bal = Balance{}, int ctas = 0) {
   using G = v3::Cfg<DK, STAGES>;
   static_assert(G::SMEM <= 227 * 1024, "shared memory budget");
-  auto kern = bal.on ? v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC, true>
-                     : v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC, false>;
+  const bool padk = s.dk != DK;
+  auto kern = bal.on ? (padk ? v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC, true, true>
+                             : v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC, true, false>)
+                     : (padk ? v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC, false, true>
+                             : v3::prefill_tc_tmem_state_kernel<DK, STAGES, MC, false, false>);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
@@ -1382,7 +1424,7 @@ cudaError_t launch_tmem_state_mc(const CUtensorMap& mq, const CUtensorMap& mk, c
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = bal.on ? 1 : 2;
-  err = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H, (int)s.N, (int)s.dv,
+  err = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, log2g, s_in, s_out, (int)s.H, (int)s.N, (int)s.dv, (int)s.dk,
                            state_only ? 1 : 0, sa, bal, g_trace);
   count_launch();
   if (err != cudaSuccess) return err;
@@ -1413,11 +1455,11 @@ int max_active_clusters(int m) {
   int n = 0;
   cudaError_t err = cudaErrorInvalidValue;
   if (m == 4) {
-    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 4, false>;
+    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 4, false, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) == cudaSuccess)
       err = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
   } else if (m == 2) {
-    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 2, false>;
+    auto kern = v3::prefill_tc_tmem_state_kernel<DK, STAGES, 2, false, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) == cudaSuccess)
       err = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
   }
@@ -1479,10 +1521,14 @@ void set_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
 #define V2_STAGES128 4
 #endif
 
+// Any dk <= 256 and dv with 16-byte rows: the kernel for the next DK in {64, 128, 256} runs,
+// its Q/K boxes past dk zero-filled by TMA (the extra state columns stay exactly zero, and the
+// OOB fill costs no HBM traffic); V boxes past dv are zero-filled and output stores clipped.
+int tc_bucket(int64_t dk) { return dk <= 64 ? 64 : dk <= 128 ? 128 : 256; }
+
 bool tc_supported(const ShapeArgs& s, int dtype) {
   if (dtype != LINATTN_BF16) return false;
-  if (!(s.dk == 64 || s.dk == 128 || s.dk == 256)) return false;
-  if (s.dv % 64 != 0) return false;
+  if (s.dk < 1 || s.dk > 256 || s.dk % 8 != 0 || s.dv % 8 != 0) return false;
   return encode_fn() != nullptr;
 }
 
@@ -1492,7 +1538,7 @@ cudaError_t launch_prefill_tc(const void* q, const void* k, const void* v, void*
                               cudaStream_t stream) {
   for (const void* p : {q, k, v, (const void*)o})
     if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return cudaErrorNotSupported;
-  switch (s.dk) {
+  switch (tc_bucket(s.dk)) {
     case 64:
       if (state_only) return launch_pipe<64, 8, true>(q, k, v, o, log2g, s_in, s_out, s, true, sa, nz, stream);
       return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, false, sa, nz, stream);
@@ -1518,19 +1564,19 @@ __global__ void gamma_tables_kernel(const float* __restrict__ log2g, float* __re
 }
 // [ctas] hand-off flags, the ticket counter, then [ctas] per-cluster ticket slots
 size_t flags_bytes(int ctas) { return 256 * (size_t)((2 * ctas + 1 + 63) / 64); }
-size_t tab_bytes(const ShapeArgs& s) { return s.dk == 256 ? 256 * (size_t)((s.H * 257 * 4 + 255) / 256) : 0; }
+size_t tab_bytes(const ShapeArgs& s) { return tc_bucket(s.dk) == 256 ? 256 * (size_t)((s.H * 257 * 4 + 255) / 256) : 0; }
 }  // namespace
 
 int tc_balance_ctas(const ShapeArgs& s, int sms, int env) {
   const int64_t tiles = (s.dv + kDVT - 1) / kDVT;
-  if (s.dk <= 128) {
+  if (tc_bucket(s.dk) <= 128) {
     const int64_t units = s.B * s.H * tiles, rem = units % sms;
     if (units <= sms || rem == 0) return 0;
     // a last wave more than half full already streams near the HBM roofline (each CTA is bound
     // by its own serial chunk chain, so fewer CTAs each go faster)
     return (env > 0 || 2 * rem <= sms) ? sms : 0;
   }
-  if (s.dk != 256 || tiles % 2 != 0) return 0;
+  if (tiles % 2 != 0) return 0;
   // dk = 256: ranges over clusters of two CTAs (74 co-resident pairs, all SMs) against the
   // plain grid's whole waves of the best cluster size (33 co-resident quads)
   const int slots2 = max_active_clusters<256, 2>(2);
@@ -1551,7 +1597,7 @@ int tc_balance_ctas(const ShapeArgs& s, int sms, int env) {
 }
 
 size_t balance_workspace_bytes(const ShapeArgs& s, int ctas) {
-  return flags_bytes(ctas) + tab_bytes(s) + (size_t)ctas * s.dk * kDVT * sizeof(float);
+  return flags_bytes(ctas) + tab_bytes(s) + (size_t)ctas * tc_bucket(s.dk) * kDVT * sizeof(float);
 }
 
 cudaError_t launch_prefill_tc_balanced(const void* q, const void* k, const void* v, void* o,
@@ -1559,13 +1605,14 @@ cudaError_t launch_prefill_tc_balanced(const void* q, const void* k, const void*
                                        const ShapeArgs& s, int ctas, void* ws, cudaStream_t stream) {
   for (const void* p : {q, k, v, (const void*)o})
     if (reinterpret_cast<uintptr_t>(p) & 15) return cudaErrorNotSupported;
-  const int mc = s.dk == 256 ? 2 : 1;                      // CTAs per cluster (one range each)
+  const int DKB = tc_bucket(s.dk);
+  const int mc = DKB == 256 ? 2 : 1;                       // CTAs per cluster (one range each)
   const int64_t ntiles = (s.dv + kDVT - 1) / kDVT;
   if (ntiles % mc != 0 || ctas % mc != 0) return cudaErrorNotSupported;
   const int64_t units = s.B * s.H * (ntiles / mc), nc = (s.N + kC - 1) / kC;
   const int ranges = ctas / mc;
   const int64_t w = (units * nc + ranges - 1) / ranges;
-  if ((s.dk != 64 && s.dk != 128 && s.dk != 256) || w < nc || units * nc > (1LL << 31) - 1)
+  if (!tc_supported(s, LINATTN_BF16) || w < nc || units * nc > (1LL << 31) - 1)
     return cudaErrorNotSupported;
   Balance bal;
   bal.on = 1;
@@ -1582,9 +1629,9 @@ cudaError_t launch_prefill_tc_balanced(const void* q, const void* k, const void*
   const int used = (int)((units * nc + w - 1) / w) * mc;   // CTAs whose range holds work
   cudaError_t err = cudaMemsetAsync(ws, 0, sizeof(unsigned) * (ctas + 1), stream);
   if (err != cudaSuccess) return err;
-  if (s.dk == 64)
+  if (DKB == 64)
     return launch_pipe<64, 6>(q, k, v, o, log2g, s_in, s_out, s, false, SegArgs{}, 1, stream, bal, used);
-  if (s.dk == 128)
+  if (DKB == 128)
     return launch_pipe<128, V2_STAGES128>(q, k, v, o, log2g, s_in, s_out, s, false, SegArgs{}, 1, stream, bal, used);
   gamma_tables_kernel<<<(unsigned)s.H, 64, 0, stream>>>(log2g, tab);
   count_launch();

@@ -15,7 +15,7 @@ namespace {
 constexpr int MAXP = 64;
 constexpr int kLoads = 8;          // entries loaded ahead per thread
 struct SegLens {
-  float len[MAXP];
+  long long len[MAXP];   // segment lengths in tokens (int64: exact past 2^24)
 };
 
 __global__ void prefix_combine_kernel(const float4* __restrict__ gathered, float4* __restrict__ s_in,
@@ -35,7 +35,7 @@ __global__ void prefix_combine_kernel(const float4* __restrict__ gathered, float
 #pragma unroll
     for (int j = 0; j < kLoads; ++j) {
       if (p0 + j >= rank) break;
-      const float c = gpow(lg, lens.len[p0 + j]);
+      const float c = gpow_n(lg, lens.len[p0 + j]);
       acc.x = fmaf(c, acc.x, x[j].x);
       acc.y = fmaf(c, acc.y, x[j].y);
       acc.z = fmaf(c, acc.z, x[j].z);
@@ -61,7 +61,7 @@ __global__ void prefix_combine_kernel_scalar(const float* __restrict__ gathered,
       if (p0 + j < rank) x[j] = gathered[(int64_t)(p0 + j) * per_rank + idx];
 #pragma unroll
     for (int j = 0; j < kLoads; ++j)
-      if (p0 + j < rank) acc = fmaf(gpow(lg, lens.len[p0 + j]), acc, x[j]);
+      if (p0 + j < rank) acc = fmaf(gpow_n(lg, lens.len[p0 + j]), acc, x[j]);
   }
   s_in[idx] = acc;
 }
@@ -181,7 +181,7 @@ cudaError_t launch_prefix_combine(const float* gathered, float* s_in, const int6
                                   cudaStream_t stream) {
   if (P > MAXP || rank < 0 || rank >= P) return cudaErrorInvalidValue;
   SegLens lens{};
-  for (int p = 0; p < P; ++p) lens.len[p] = (float)seg_lens[p];
+  for (int p = 0; p < P; ++p) lens.len[p] = (long long)seg_lens[p];
   const int64_t per_head = s.dk * s.dv;
   const int64_t per_rank = s.B * s.H * per_head;
   const bool vec = (per_head % 4 == 0) && ((reinterpret_cast<uintptr_t>(gathered) & 15) == 0) &&

@@ -147,14 +147,20 @@ def _seqpar(q, k, v, log2g, parts: int, kernel: str):
 
 
 def _recurrent(q, k, v, log2g):
-    """Row-based route (kernels.py:93-106): one launch walks every token with the state on chip;
-    shapes the scan kernel does not take (rows not a multiple of 16 bytes, dk > 256) step the
-    decode kernel per token."""
+    """Row-based route (kernels.py:93-106): one launch walks every token with the state on chip.
+    Rows that are not a multiple of 16 bytes are zero-padded to one (zero k columns leave the
+    extra state rows at zero, the extra v columns are dropped); only dk > 256, past the scan
+    kernel's state budget, steps the decode kernel per token."""
     B, H, N, dk = q.shape
     dv = v.shape[3]
     ev = 16 // q.element_size()
-    if dk % ev == 0 and dv % ev == 0 and dk <= 256:
-        return ops.recurrent(q, k, v, log2g)
+    if dk <= 256:
+        if dk % ev == 0 and dv % ev == 0:
+            return ops.recurrent(q, k, v, log2g)
+        pk, pv = -(-dk // ev) * ev - dk, -(-dv // ev) * ev - dv
+        pad = torch.nn.functional.pad
+        out = ops.recurrent(pad(q, (0, pk)), pad(k, (0, pk)), pad(v, (0, pv)), log2g)
+        return out[..., :dv].contiguous()
     state = torch.zeros((B, H, dk, dv), dtype=torch.float32, device=q.device)
     out = torch.empty_like(v)
     for i in range(N):

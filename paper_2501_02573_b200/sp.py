@@ -91,7 +91,7 @@ def sp_prefill(q_seg, k_seg, v_seg, log2g, seg_lens, group=None, backend=None):
     if k_seg.shape[2] != seg_lens[rank]:
         raise ValueError(f"rank {rank} holds {k_seg.shape[2]} tokens, seg_lens says {seg_lens[rank]}")
     local_data, local = backend.local_states(k_seg, v_seg, log2g)   # end state from zero [B,H,dk,dv]
-    if world > 1:
+    if dist.is_initialized():   # the collective runs under any group (world 1 included: one code path)
         local = local.contiguous()
         # gloo has no device all-gather: stage through the host (CPU tests, shared-GPU path checks)
         host = local.is_cuda and dist.get_backend(group) == "gloo"

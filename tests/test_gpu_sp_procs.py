@@ -56,3 +56,30 @@ def test_sp_prefill_processes_on_device(tmp_path, world, n):
     res = str(tmp_path / "err.npy")
     mp.spawn(_worker, args=(world, _free_port(), n, res), nprocs=world, join=True)
     assert float(np.load(res)[0]) <= 2e-2
+
+
+def _nccl_worker(rank, port, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    from paper_2501_02573_b200 import ops
+    from paper_2501_02573_b200.sp import sp_prefill
+    b, c, v = orc.gen_inputs(1, 4, 5000, 128, 128, np.float32, 29)
+    b, c, v = orc.bf16_round(b), orc.bf16_round(c), orc.bf16_round(v)
+    gam = [1 - 2.0 ** -6, 1 - 2.0 ** -13, 0.5, 1.0]
+    x = [torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.bfloat16) for a in (b, c, v)]
+    out = sp_prefill(*x, ops.log2_gamma(gam, True, "cuda"), [5000]).float().cpu().numpy()
+    np.save(result_path, np.array([orc.max_rel_error(out, orc.oracle_attn(b, c, v, gam, True))]))
+    dist.destroy_process_group()
+
+
+def test_sp_prefill_nccl_group(tmp_path):
+    """The NCCL code path of sp_prefill (all_gather_into_tensor of the fp32 end states on the
+    device, no host staging) on a one-rank NCCL group: the box has one GPU and NCCL allows one
+    rank per device, so this is the largest NCCL group a test can build here."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    res = str(tmp_path / "err.npy")
+    mp.spawn(_nccl_worker, args=(_free_port(), res), nprocs=1, join=True)
+    assert float(np.load(res)[0]) <= 2e-2
