@@ -34,5 +34,23 @@ q = torch.randn(1, 40, 200, 256, device="cuda", dtype=torch.bfloat16)
 k = torch.randn_like(q)
 v = torch.randn(1, 40, 200, 512, device="cuda", dtype=torch.bfloat16)
 ops.prefill(q, k, v, ops.log2_gamma([0.9] * 40, True, "cuda"), s_out=torch.empty(1, 40, 256, 512, device="cuda"))
+# any head width on the tensor cores (padded DK instantiations, dv not a multiple of 32 / 64),
+# with initial and end states, the state pass and the in-device split
+for (B, H, N, dk, dv) in [(2, 3, 333, 96, 72), (1, 2, 200, 200, 40), (1, 1, 150, 24, 8)]:
+    q = torch.randn(B, H, N, dk, device="cuda", dtype=torch.bfloat16)
+    k = torch.randn_like(q)
+    v = torch.randn(B, H, N, dv, device="cuda", dtype=torch.bfloat16)
+    l2 = ops.log2_gamma([0.9] * H, True, "cuda")
+    ops.prefill(q, k, v, l2, s_in=torch.zeros(B, H, dk, dv, device="cuda"),
+                s_out=torch.empty(B, H, dk, dv, device="cuda"), kernel="tc")
+    ops.state_pass(k, v, l2, kernel="tc")
+    ops.prefill(q, k, v, l2, seq_split=2, kernel="tc")
+# fp32 parity mode on the tensor cores (3xTF32) and the row recurrence
+q = torch.randn(2, 3, 300, 128, device="cuda")
+k = torch.randn_like(q)
+v = torch.randn(2, 3, 300, 128, device="cuda")
+l2 = ops.log2_gamma([0.9] * 3, True, "cuda")
+ops.prefill(q, k, v, l2, s_out=torch.empty(2, 3, 128, 128, device="cuda"), kernel="tf32")
+ops.recurrent(q, k, v, l2, s_out=torch.empty(2, 3, 128, 128, device="cuda"))
 torch.cuda.synchronize()
 print("sanitize driver done")
