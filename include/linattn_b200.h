@@ -66,7 +66,8 @@ typedef enum { LINATTN_F32 = 0, LINATTN_BF16 = 1 } linattn_dtype;
 /* Kernel family selector for linattn_prefill / linattn_state_pass. */
 typedef enum {
   LINATTN_KERNEL_AUTO = 0, /* bf16 -> TC, f32 -> TF32 when the shape/alignment allows, else SIMT */
-  LINATTN_KERNEL_TC = 1,   /* tcgen05 + TMA chunked kernel (bf16 only); EUNSUPPORTED otherwise */
+  LINATTN_KERNEL_TC = 1,   /* tcgen05 + TMA chunked kernel: bf16, dk <= 256, dk and dv multiples of 8;
+                              EUNSUPPORTED otherwise */
   LINATTN_KERNEL_SIMT = 2, /* fp32-FFMA chunked kernel (f32 or bf16; any dk, dv) */
   LINATTN_KERNEL_TF32 = 3  /* tcgen05 kind::tf32 3xTF32 chunked kernel, the f32 parity mode on the
                               tensor cores (f32, dk <= 128, dk and dv multiples of 4) */
