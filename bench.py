@@ -94,7 +94,7 @@ def _slice_inputs(sid, n, dk, dv, gamma):
     return b, c, v, gamma
 
 
-def _ref_worker(conn, sids, n, dk, dv, gammas, use_ref):
+def _ref_worker(conn, sids, n, dk, dv, gammas, use_ref, method_name=REF_METHOD):
     """Pool worker: builds its slices' inputs (untimed), then times run_method per command."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     try:
@@ -104,7 +104,7 @@ def _ref_worker(conn, sids, n, dk, dv, gammas, use_ref):
         pass
     lib = _import_reference() if use_ref else None
     if lib is not None:
-        method = lib.MethodId.parse(REF_METHOD)
+        method = lib.MethodId.parse(method_name)
         params = lib.BlockParams()
         inputs = []
         for sid in sids:
@@ -115,7 +115,11 @@ def _ref_worker(conn, sids, n, dk, dv, gammas, use_ref):
     else:
         from oracle import linattn_oracle as orc
         inputs = [_slice_inputs(sid, n, dk, dv, gammas[sid % len(gammas)]) for sid in sids]
-        run = lambda inp: orc.blocked_attn(inp[0], inp[1], inp[2], [inp[3]], True, block=C0)   # noqa: E731
+        if method_name == "row-based":
+            run = lambda inp: orc.row_recurrence(inp[0][0, 0], inp[1][0, 0], inp[2][0, 0], inp[3], True,  # noqa: E731
+                                                 dtype=np.float32)
+        else:
+            run = lambda inp: orc.blocked_attn(inp[0], inp[1], inp[2], [inp[3]], True, block=C0)   # noqa: E731
     conn.send("ready")
     while True:
         cmd = conn.recv()
@@ -133,7 +137,7 @@ def _ref_worker(conn, sids, n, dk, dv, gammas, use_ref):
 class RefPool:
     """One worker process per core, each owning a fixed share of the (b, h) slices."""
 
-    def __init__(self, slices, workers, n, dk, dv, gammas, use_ref):
+    def __init__(self, slices, workers, n, dk, dv, gammas, use_ref, method_name=REF_METHOD):
         ctx = mproc.get_context("spawn")
         self.conns, self.procs = [], []
         os.environ["OPENBLAS_NUM_THREADS"] = "1"          # inherited by the spawned workers
@@ -142,7 +146,8 @@ class RefPool:
             if not mine:
                 continue
             a, b = ctx.Pipe()
-            p = ctx.Process(target=_ref_worker, args=(b, mine, n, dk, dv, gammas, use_ref), daemon=True)
+            p = ctx.Process(target=_ref_worker, args=(b, mine, n, dk, dv, gammas, use_ref, method_name),
+                            daemon=True)
             p.start()
             self.conns.append(a)
             self.procs.append(p)
@@ -236,6 +241,31 @@ def cpu_arm(steps, warmup, seconds=None):
         except Exception as exc:  # informational only
             out["as_shipped"] = {"error": repr(exc)}
     return out
+
+
+def cpu_decode_arm(sample=64):
+    """The reference's row recurrence (run_method(row-based), kernels.py:93-106: the per-token
+    decode update S <- gamma S + k^T v, o = q S) on `sample` of the 8192 configs[3] states for
+    1024 tokens each, over one worker process per core; extrapolated linearly to one decode step
+    of all 8192 states (the states are independent, kernels.py:273-280)."""
+    lib = _import_reference()
+    cores = cores_available()
+    states = DEC["B"] * DEC["H"]
+    pool = RefPool(sample, cores, DEC["steps"], DEC["dk"], DEC["dv"], gammas(DEC["H"]), lib is not None,
+                   method_name="row-based")
+    try:
+        pool.step()                                           # warm-up
+        wall, per = pool.step()
+    finally:
+        pool.close()
+    us = wall / DEC["steps"] * (states / sample) * 1e6
+    return {"us_per_step": us, "cores": len(pool.conns), "kind": "reference" if lib is not None else "port",
+            "per_state_token_us": 1e6 * float(np.mean(per)) / DEC["steps"],
+            "sample": (f"{sample} of {states} (b,h) states x {DEC['steps']} tokens, d={DEC['dk']} f32, "
+                       + ("linattn.run_method(row-based, validate=False) from baseline/_ref"
+                          if lib is not None else "oracle port of the row recurrence")
+                       + f", {len(pool.conns)} worker processes x 1 BLAS thread; one decode step of all "
+                         f"{states} states extrapolated linearly")}
 
 
 def cores_available():
@@ -649,6 +679,8 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_arm(0, 1, seconds=args.cpu_seconds)
+        if dec is not None:
+            dec["cpu_baseline"] = cpu_decode_arm()
 
     kernel_name = ops.prefill_kernel_name(dk, dv, torch.bfloat16, kernel)
     line = {
