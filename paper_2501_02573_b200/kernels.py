@@ -35,7 +35,7 @@ import numpy as np
 import torch
 
 from . import ops
-from .errors import LinAttnError, UsageError
+from .errors import LinAttnError, ResourceError, UsageError
 from .tensor import (DEFER, AttnInputs, check_finite_all, check_output_then_inputs, finite_check_pending,
                      mark_finite, validate_inputs)
 
@@ -319,7 +319,17 @@ def run_method(method: MethodId, inputs: AttnInputs, params: BlockParams | None 
     ``out`` (optional, not in the reference signature) is a caller-owned result
     buffer of the input's shape and dtype -- e.g. a pinned host tensor, so the
     device->host copy of a host-tensor call runs at full PCIe bandwidth.
+    Device memory exhaustion raises the reference's ``ResourceError`` (errors.py:25; the
+    reference raises it when a buffer would exceed its byte cap), so ``run_bench`` records an
+    OOM row and carries on exactly as it does for the reference's capped methods.
     """
+    try:
+        return _run_method(method, inputs, params, validate, out)
+    except torch.OutOfMemoryError as exc:
+        raise ResourceError(f"device memory exhausted running {method}: {str(exc).splitlines()[0]}") from exc
+
+
+def _run_method(method, inputs, params, validate, out):
     if isinstance(method, str):
         method = MethodId.parse(method)
     if method is MethodId.AUTO:

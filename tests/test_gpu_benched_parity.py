@@ -257,3 +257,25 @@ def test_tensors_on_non_current_device(ops):
     out = ops.prefill(q, k, vv, l2)
     assert out.device == dev
     assert orc.max_rel_error(out.float().cpu().numpy(), orc.oracle_attn(b, c, v, [0.9, 1.0], True)) <= TOL_BF16
+
+
+def test_device_oom_is_resource_error(ops):
+    """Device memory exhaustion surfaces as the reference's ResourceError (errors.py:25), and the
+    package run_bench turns it into an OOM row (reference bench.py:116-117) and carries on."""
+    import paper_2501_02573_b200 as la
+    from paper_2501_02573_b200.bench import BenchConfig, run_bench
+    free, total = torch.cuda.mem_get_info()
+    torch.cuda.empty_cache()
+    frac = min(1.0, (torch.cuda.memory_allocated() + (64 << 20)) / total)   # ~64 MiB of headroom
+    torch.cuda.set_per_process_memory_fraction(frac)
+    try:
+        big = la.make_inputs(*(torch.ones(1, 8, 65536, 128) for _ in range(3)), gamma=[0.9] * 8)
+        with pytest.raises(la.ResourceError):
+            la.run_method(la.MethodId.B200_CHUNKED, big)
+        cfg = BenchConfig(methods=[la.MethodId.B200_CHUNKED], grid=[(1, 8, 65536, 128, 128), (1, 2, 256, 64, 64)],
+                          repeats=1, warmup=0)
+        rows = {r.seqlen: r for r in run_bench(cfg).rows}
+        assert rows[65536].status == "OOM" and rows[256].status == "ok"
+    finally:
+        torch.cuda.set_per_process_memory_fraction(1.0)
+        torch.cuda.empty_cache()
