@@ -227,6 +227,7 @@ cudaError_t launch_prefill_tc_balanced(const void* q, const void* k, const void*
                                        const float* log2g, const float* s_in, float* s_out,
                                        const ShapeArgs& s, int ctas, void* ws, cudaStream_t stream);
 void set_trace(void* buf);  // debug only: per-chunk clock64 trace of CTA (0,0), nullptr = off
+unsigned long long* trace_buffer();   // the buffer set_trace installed (nullptr = off)
 
 // Whole-sequence row recurrence in one launch (reference _row_based_slice, kernels.py:93-106).
 cudaError_t launch_recurrent(const void* q, const void* k, const void* v, void* o, const float* log2g,

@@ -1516,6 +1516,7 @@ cudaError_t launch_tmem_state(const void* q, const void* k, const void* v, void*
 }  // namespace
 
 void set_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
+unsigned long long* trace_buffer() { return g_trace; }
 
 #ifndef V2_STAGES128
 #define V2_STAGES128 4

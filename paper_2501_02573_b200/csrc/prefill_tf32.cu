@@ -52,6 +52,9 @@
 #ifndef TF32_BAL_PDL
 #define TF32_BAL_PDL 0
 #endif
+#ifndef TF32_TRACE
+#define TF32_TRACE 0           // dev: per-chunk clock64 timeline of CTA (0,0,0) (tools/trace_tf32.py)
+#endif
 #ifndef TF32_L2_PREFETCH
 #define TF32_L2_PREFETCH 1     // warm L2 with the chunk that will reuse a K|V stage
 #endif
@@ -110,7 +113,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, float* __restrict__ o,
                     const float* __restrict__ log2g, const float* __restrict__ s_in, float* __restrict__ s_out,
-                    int H, int N, int dk, int dv, const SegArgs sa, const Balance bal, float* __restrict__ dump) {
+                    int H, int N, int dk, int dv, const SegArgs sa, const Balance bal, float* __restrict__ dump,
+                    unsigned long long* __restrict__ trace) {
   using G = Cfg<DKP, QST, KVST>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // aligned by pointer arithmetic (not via an integer cast) so ptxas keeps the shared address
@@ -223,6 +227,13 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     named_bar_sync(bar_id, nthr);
   };
   const bool dumping = !BAL && dump != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  // debug: per-chunk clock64 of CTA (0,0,0), trace[event * 4096 + chunk] (tools/trace_tf32.py)
+  const bool tracing = !BAL && trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+#if TF32_TRACE
+#define TF_TRACE(ev, c) do { if (tracing && lane == 0 && (c) < 4096) trace[(ev) * 4096 + (c)] = clock64(); } while (0)
+#else
+#define TF_TRACE(ev, c) do { (void)tracing; } while (0)   // build with -DTF32_TRACE=1 (tools/build_variant.sh)
+#endif
 
   if (warp < 2) {
     // ------------------------------------------------------------ P^T mask + hi/lo split
@@ -273,6 +284,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           fence_proxy_async_smem();
           tc_fence_before();
           mbar_arrive(mask_bar);
+          if (warp == 0) TF_TRACE(9, gc);
         }
       }
     }
@@ -312,6 +324,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         fence_proxy_async_smem();
         mbar_arrive(&prepA[b]);
+        if (warp == 2) TF_TRACE(10, gc);
       }
       if (gc > 0) mbar_wait(derB_free, (gc - 1) & 1);
       // Row units (a 128-byte row of one 32-column box): K' = gamma^(L-1-s) K (zero past the ragged
@@ -376,6 +389,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
       }
       mbar_arrive(prepB);
+      if (warp == 2) TF_TRACE(11, gc);
      }
     }
   } else if (warp < 12) {
@@ -451,6 +465,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const int L = min(kC, w.hi - w.lo - c * kC);
         mbar_wait(mma_s_bar, gc & 1);
         tc_fence_after();
+        if (warp == 4) TF_TRACE(0, gc);
         const float carry = pw_st[L];
 #pragma unroll
         for (int j = 0; j < SC / 16; ++j) {
@@ -464,10 +479,13 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         tc_fence_before();
         mbar_arrive(ds_free);
+        if (warp == 4) TF_TRACE(1, gc);
         if (SO) continue;
         mbar_wait(mma_o_bar, gc & 1);                 // Oi, Ox done: S hi/lo may be replaced
         tc_fence_after();
+        if (warp == 4) TF_TRACE(2, gc);
         if (c != nch - 1) publish();
+        if (warp == 4) TF_TRACE(3, gc);
         // ---- outputs: O[t][d] = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t], tokens g*16 .. g*16+15;
         //      for each t the 32 lanes of a warp store 32 consecutive dv columns (128 B)
         float ov[16], xv[16];
@@ -476,6 +494,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(o_free);
+        if (warp == 4) TF_TRACE(4, gc);
         if (dv_ok) {
           float* orc = orow + (size_t)(c * kC + g * 16) * dv;
 #pragma unroll
@@ -548,6 +567,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             for (int kb = 0; kb < G::KB; ++kb) tma_load_3d(qd + kb * 4096, &tm_q, &full_q[sq], kb * 32, t0, w.bh);
           }
           mbar_wait(&empty_kv[skv], ((gc / KVST) & 1) ^ 1);
+          TF_TRACE(12, gc);
           uint8_t* kd = smem + G::OFF_KV + skv * G::KV_BYTES;
           mbar_arrive_expect_tx(&full_kv[skv], G::KV_BYTES);
 #pragma unroll
@@ -601,6 +621,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
       mma_commit_elect(mma1_bar);
       mma_commit_elect(klo_free);
+      TF_TRACE(7, c);
     };
     if (!SO && nchunks > 0) issue_mma1(0);
     for (int c = 0; c < nchunks; ++c) {
@@ -608,10 +629,12 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       const uint64_t q_k = dK0 + sq * kQK;                            // raw Q (hi), K-major
       const uint64_t qlo_k = qlo_k0 + (c & 1) * kQK;
       const uint64_t v_m = kv_m0 + skv * kKV + kQK;                   // V (hi), MN-major
+      TF_TRACE(13, c);
       mbar_wait(&full_kv[skv], (c / KVST) & 1);
       mbar_wait(prepB, c & 1);
       if (c > 0) mbar_wait(ds_free, (c - 1) & 1);
       tc_fence_after();
+      TF_TRACE(5, c);
       // dS^T = Vhi K'hi + Vhi K'lo + Vlo K'hi   (K step = 8 token rows = 1 KiB)
 #pragma unroll
       for (int ks = 0; ks < kC / 8; ++ks) {
@@ -634,6 +657,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           mma_tf32_ss_elect(tbase + T_O, vlo_m + off, ph_m + off, id_vp, 1);
         }
         mma_commit_elect(p_free);
+        TF_TRACE(6, c);
         mma_commit_elect(derB_free);
         mma_commit_elect(&empty_kv[skv]);            // K (MMA1, K') and V (dS, Oi) consumed
         if (c + 1 < nchunks) issue_mma1(c + 1);
@@ -651,6 +675,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             mma_tf32_ts_elect(tbase + T_OX, tbase + T_SLO + col, q_k + off, id_sq, 1);
           }
         mma_commit_elect(mma_o_bar);
+        TF_TRACE(8, c);
         mma_commit_elect(&derA_free[c & 1]);
         mma_commit_elect(&empty_q[sq]);
       } else {
@@ -705,12 +730,13 @@ cudaError_t launch_v4(const void* q, const void* k, const void* v, void* o, cons
   if constexpr (BAL && !TF32_BAL_PDL) {   // follows the memset of its flags: plain stream order
     kern<<<dim3((unsigned)ctas), v4::kThreads, G::SMEM, stream>>>(mq, mk, mv, static_cast<float*>(o), log2g, s_in,
                                                                   s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv,
-                                                                  sa, bal, nullptr);
+                                                                  sa, bal, nullptr, nullptr);
   } else {
     const dim3 grid = BAL ? dim3((unsigned)ctas)
                           : dim3((unsigned)((s.dv + v4::kDVT - 1) / v4::kDVT), (unsigned)BH, (unsigned)nz);
     err = launch_pdl(kern, grid, dim3(v4::kThreads), G::SMEM, stream, mq, mk, mv, static_cast<float*>(o), log2g,
-                     s_in, s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, sa, bal, g_tf32_dump);
+                     s_in, s_out, (int)s.H, (int)s.N, (int)s.dk, (int)s.dv, sa, bal, g_tf32_dump,
+                     BAL ? nullptr : trace_buffer());
     if (err != cudaSuccess) return err;
   }
   count_launch();
