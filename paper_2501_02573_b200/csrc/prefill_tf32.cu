@@ -52,6 +52,9 @@
 #ifndef TF32_BAL_PDL
 #define TF32_BAL_PDL 0
 #endif
+#ifndef TF32_FUSE_DS_OI
+#define TF32_FUSE_DS_OI 1      // dS^T = V^T K' and Oi^T = V^T P^T as one N = dk + 32 MMA group (V^T read once)
+#endif
 #ifndef TF32_TRACE
 #define TF32_TRACE 0           // dev: per-chunk clock64 timeline of CTA (0,0,0) (tools/trace_tf32.py)
 #endif
@@ -79,7 +82,8 @@ constexpr int kDVT = 128;        // dv rows per CTA (MMA M)
 constexpr int kThreads = 512;
 constexpr int kPrep = 128;       // operand-prep threads (warps 2, 3, 14, 15)
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t T_P = 0, T_OX = 32, T_O = 64, T_DS = 128, T_SHI = 256, T_SLO = 384;
+// dS (dk columns) and O_intra (32) are adjacent, so one MMA group with B = [K' | P^T] fills both
+constexpr uint32_t T_P = 0, T_OX = 32, T_DS = 64, T_O = 224, T_SHI = 256, T_SLO = 384;
 
 // Shared memory (1 KiB aligned).  Q/K/V tiles are TMA boxes of [32 rows][32 fp32] (4 KiB, 128-byte
 // swizzle), column blocks 4 KiB apart.  MMA1 reads K as a 128-row A operand (rows 32..127 are
@@ -95,11 +99,14 @@ struct Cfg {
   static constexpr int OFF_KV = QST * QK_BYTES;
   static constexpr int OFF_KLO = OFF_KV + KVST * KV_BYTES;         // Klo | Qlo[2], K-major
   static constexpr int OFF_QLO = OFF_KLO + QK_BYTES;
-  static constexpr int OFF_KPH = OFF_QLO + 2 * QK_BYTES;           // K'hi | K'lo | Vlo, MN-major
-  static constexpr int OFF_KPL = OFF_KPH + QK_BYTES;
-  static constexpr int OFF_VLO = OFF_KPL + QK_BYTES;
-  static constexpr int OFF_P = OFF_VLO + V_BYTES;                  // P^T hi | lo [32 s][32 t]
-  static constexpr int OFF_POW = OFF_P + 2 * 4096;                 // gamma^n, n = 0..32
+  // MN-major tf32 tiles, 32-column blocks 4 KiB apart: [K'hi | P^T hi] and [K'lo | P^T lo] are
+  // each one contiguous B operand of N = dk + 32 (P^T [32 s][32 t]), then Vlo
+  static constexpr int OFF_KPH = OFF_QLO + 2 * QK_BYTES;
+  static constexpr int OFF_PH = OFF_KPH + QK_BYTES;
+  static constexpr int OFF_KPL = OFF_PH + 4096;
+  static constexpr int OFF_PL = OFF_KPL + QK_BYTES;
+  static constexpr int OFF_VLO = OFF_PL + 4096;
+  static constexpr int OFF_POW = OFF_VLO + V_BYTES;                // gamma^n, n = 0..32
   static constexpr int OFF_BAR = OFF_POW + 3 * 64 * 4;            // (three per-role tables)
   static constexpr int SMEM = OFF_BAR + 512 + 1024;
   // the 64-row A operand of MMA1 reads 4 KiB past the last K box (K then V in a K|V stage, Klo then Qlo)
@@ -116,6 +123,9 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     int H, int N, int dk, int dv, const SegArgs sa, const Balance bal, float* __restrict__ dump,
                     unsigned long long* __restrict__ trace) {
   using G = Cfg<DKP, QST, KVST>;
+  // O_intra accumulator: right after the dk columns of dS (the fused [dS | Oi] group writes both)
+  constexpr uint32_t T_OI = TF32_FUSE_DS_OI ? T_DS + DKP : T_O;
+  static_assert(T_OI + kC <= T_SHI, "TMEM columns");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // aligned by pointer arithmetic (not via an integer cast) so ptxas keeps the shared address
   // space: LDS/STS instead of generic loads/stores
@@ -241,8 +251,8 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (!SO) {
       const int srow = 16 * (int)warp + (int)(lane & 15);
       const bool live = lane < 16;
-      uint8_t* ph = smem + G::OFF_P;
-      uint8_t* pl = ph + 4096;
+      uint8_t* ph = smem + G::OFF_PH;
+      uint8_t* pl = smem + G::OFF_PL;
       int gc = 0;
       for (int it = 0; it < nitems; ++it) {
         const WorkItem w = item(it);
@@ -489,7 +499,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         // ---- outputs: O[t][d] = Oi^T[d][t] + gamma^(t+1) Ox^T[d][t], tokens g*16 .. g*16+15;
         //      for each t the 32 lanes of a warp store 32 consecutive dv columns (128 B)
         float ov[16], xv[16];
-        tmem_ld16(lane_base + T_O + g * 16, ov);
+        tmem_ld16(lane_base + T_OI + g * 16, ov);
         tmem_ld16(lane_base + T_OX + g * 16, xv);
         tmem_wait_ld();
         tc_fence_before();
@@ -585,6 +595,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     // stream across the work list (only buffer/stage indices depend on the chunk).
     constexpr uint32_t id_qk = idesc_tf32(64, kC, false, false);     // P^T = K Q^T (M = 64)
     constexpr uint32_t id_vk = idesc_tf32(128, DKP, true, true);     // dS^T = V^T K'
+    constexpr uint32_t id_vkp = idesc_tf32(128, DKP + kC, true, true);   // [dS^T | Oi^T] = V^T [K' | P^T]
     constexpr uint32_t id_vp = idesc_tf32(128, kC, true, true);      // Oi^T = V^T P^T
     constexpr uint32_t id_sq = idesc_tf32(128, kC, false, false);    // Ox^T = S^T(TMEM) Q^T
     const uint32_t base = smem_u32(smem);
@@ -595,7 +606,7 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const uint64_t kv_k0 = dK0 + (G::OFF_KV >> 4), kv_m0 = dM0 + (G::OFF_KV >> 4);
     const uint64_t kph_m = dM0 + (G::OFF_KPH >> 4), kpl_m = dM0 + (G::OFF_KPL >> 4);
     const uint64_t vlo_m = dM0 + (G::OFF_VLO >> 4);
-    const uint64_t ph_m = dM0 + (G::OFF_P >> 4), pl_m = ph_m + (4096 >> 4);
+    const uint64_t ph_m = dM0 + (G::OFF_PH >> 4), pl_m = dM0 + (G::OFF_PL >> 4);
     int nchunks = 0;
     for (int it = 0; it < nitems; ++it) nchunks += item_chunks(item(it));
     // a lane-0 broadcast makes the chunk count (and every descriptor derived from the chunk
@@ -633,28 +644,48 @@ prefill_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       mbar_wait(&full_kv[skv], (c / KVST) & 1);
       mbar_wait(prepB, c & 1);
       if (c > 0) mbar_wait(ds_free, (c - 1) & 1);
-      tc_fence_after();
-      TF_TRACE(5, c);
-      // dS^T = Vhi K'hi + Vhi K'lo + Vlo K'hi   (K step = 8 token rows = 1 KiB)
-#pragma unroll
-      for (int ks = 0; ks < kC / 8; ++ks) {
-        const uint64_t off = ks * 64;
-        mma_tf32_ss_elect(tbase + T_DS, v_m + off, kph_m + off, id_vk, ks != 0);
-        mma_tf32_ss_elect(tbase + T_DS, v_m + off, kpl_m + off, id_vk, 1);
-        mma_tf32_ss_elect(tbase + T_DS, vlo_m + off, kph_m + off, id_vk, 1);
-      }
-      mma_commit_elect(mma_s_bar);
-      if (!SO) {
+      const bool fuse = TF32_FUSE_DS_OI && !SO;
+      if (fuse) {                                      // the fused group also writes O_intra and reads P^T
         mbar_wait(mask_bar, c & 1);
         if (c > 0) mbar_wait(o_free, (c - 1) & 1);
-        tc_fence_after();
-        // Oi^T = Vhi Phi + Vhi Plo + Vlo Phi
+      }
+      tc_fence_after();
+      TF_TRACE(5, c);
+      if (fuse) {
+        // [dS^T | Oi^T] = V^T [K' | P^T]: Vhi (K'|P)hi + Vhi (K'|P)lo + Vlo (K'|P)hi -- one N = dk + 32
+        // group, so V^T (hi and lo) is read from shared memory once for both products
 #pragma unroll
         for (int ks = 0; ks < kC / 8; ++ks) {
           const uint64_t off = ks * 64;
-          mma_tf32_ss_elect(tbase + T_O, v_m + off, ph_m + off, id_vp, ks != 0);
-          mma_tf32_ss_elect(tbase + T_O, v_m + off, pl_m + off, id_vp, 1);
-          mma_tf32_ss_elect(tbase + T_O, vlo_m + off, ph_m + off, id_vp, 1);
+          mma_tf32_ss_elect(tbase + T_DS, v_m + off, kph_m + off, id_vkp, ks != 0);
+          mma_tf32_ss_elect(tbase + T_DS, v_m + off, kpl_m + off, id_vkp, 1);
+          mma_tf32_ss_elect(tbase + T_DS, vlo_m + off, kph_m + off, id_vkp, 1);
+        }
+        mma_commit_elect(mma_s_bar);
+      } else {
+        // dS^T = Vhi K'hi + Vhi K'lo + Vlo K'hi   (K step = 8 token rows = 1 KiB)
+#pragma unroll
+        for (int ks = 0; ks < kC / 8; ++ks) {
+          const uint64_t off = ks * 64;
+          mma_tf32_ss_elect(tbase + T_DS, v_m + off, kph_m + off, id_vk, ks != 0);
+          mma_tf32_ss_elect(tbase + T_DS, v_m + off, kpl_m + off, id_vk, 1);
+          mma_tf32_ss_elect(tbase + T_DS, vlo_m + off, kph_m + off, id_vk, 1);
+        }
+        mma_commit_elect(mma_s_bar);
+      }
+      if (!SO) {
+        if (!fuse) {
+          mbar_wait(mask_bar, c & 1);
+          if (c > 0) mbar_wait(o_free, (c - 1) & 1);
+          tc_fence_after();
+          // Oi^T = Vhi Phi + Vhi Plo + Vlo Phi
+#pragma unroll
+          for (int ks = 0; ks < kC / 8; ++ks) {
+            const uint64_t off = ks * 64;
+            mma_tf32_ss_elect(tbase + T_OI, v_m + off, ph_m + off, id_vp, ks != 0);
+            mma_tf32_ss_elect(tbase + T_OI, v_m + off, pl_m + off, id_vp, 1);
+            mma_tf32_ss_elect(tbase + T_OI, vlo_m + off, ph_m + off, id_vp, 1);
+          }
         }
         mma_commit_elect(p_free);
         TF_TRACE(6, c);
