@@ -306,6 +306,9 @@ class ClockSampler:
 
     def __init__(self, index):
         self.index = index
+        # sampling interval: the guide's nvidia-smi recipe samples every 200 ms; every 10 ms still
+        # gives several samples inside the shortest timed region without NVML traffic at 2 ms
+        self.interval_s = float(os.environ.get("LINATTN_CLOCK_MS", "10")) / 1e3
         self.samples = []
         self.reasons = set()
         self.max_mhz = None
@@ -325,7 +328,7 @@ class ClockSampler:
                 watts = None
             self.samples.append((time.perf_counter(), mhz, mask, mem, watts))
             self._ready.set()
-            self._stop.wait(0.002)
+            self._stop.wait(self.interval_s)
 
     def __enter__(self):
         import threading
@@ -359,7 +362,8 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
                 "mem_mhz": statistics.median(mem) if mem else None,
                 "power_w_max": max(watts) if watts else None,
-                "reasons": reasons, "samples": len(sm), "source": "nvml, 2 ms, inside the timed region"}
+                "reasons": reasons, "samples": len(sm),
+                "source": f"nvml, every {self.interval_s * 1e3:g} ms, inside the timed region"}
 
 
 def load_profile_traffic(kernel_key):
