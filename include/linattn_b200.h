@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define LINATTN_ABI_VERSION 3
+#define LINATTN_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define LINATTN_API __attribute__((visibility("default")))
@@ -58,7 +58,8 @@ typedef enum {
   LINATTN_EPARAM = 2,
   LINATTN_EDTYPE = 3,
   LINATTN_EUNSUPPORTED = 4,
-  LINATTN_ECUDA = 5
+  LINATTN_ECUDA = 5,
+  LINATTN_ENOMEM = 6   /* device memory exhausted (the reference's ResourceError) */
 } linattn_status;
 
 typedef enum { LINATTN_F32 = 0, LINATTN_BF16 = 1 } linattn_dtype;

@@ -9,15 +9,15 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .errors import LinAttnError, ParameterError, ShapeError, UsageError
+from .errors import LinAttnError, ParameterError, ResourceError, ShapeError, UsageError
 
 LIB_PATH = os.environ.get("LINATTN_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "lib", "liblinattn_b200.so")  # LINATTN_LIB: dev A/B builds
 
-OK, ESHAPE, EPARAM, EDTYPE, EUNSUPPORTED, ECUDA = range(6)
+OK, ESHAPE, EPARAM, EDTYPE, EUNSUPPORTED, ECUDA, ENOMEM = range(7)
 F32, BF16 = 0, 1
 KERNEL_AUTO, KERNEL_TC, KERNEL_SIMT, KERNEL_TF32 = 0, 1, 2, 3
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _lib = None
 
@@ -83,6 +83,8 @@ def check(status: int) -> None:
         raise ParameterError(msg)
     if status in (EDTYPE, EUNSUPPORTED):
         raise UsageError(msg)
+    if status == ENOMEM:
+        raise ResourceError(msg)
     raise LinAttnError(msg or f"linattn status {status}")
 
 

@@ -39,6 +39,8 @@ static int cuda_status(cudaError_t err, const char* what) {
   if (err == cudaSuccess) return LINATTN_OK;
   if (err == cudaErrorNotSupported)
     return fail(LINATTN_EUNSUPPORTED, "%s: shape/dtype outside this kernel's envelope", what);
+  if (err == cudaErrorMemoryAllocation)
+    return fail(LINATTN_ENOMEM, "%s: device memory exhausted (%s)", what, cudaGetErrorString(err));
   return fail(LINATTN_ECUDA, "%s: CUDA error %d (%s)", what, (int)err, cudaGetErrorString(err));
 }
 
