@@ -1492,8 +1492,11 @@ cudaError_t launch_tmem_state(const void* q, const void* k, const void* v, void*
   const int64_t tiles = (s.dv + kDVT - 1) / kDVT;
   const int64_t ctas = tiles * s.B * s.H * nz;
   static const bool no_mc = getenv("LINATTN_NO_MULTICAST") != nullptr;
+  static const int force_mc = getenv("LINATTN_V3_MC") ? atoi(getenv("LINATTN_V3_MC")) : 0;   // dev A/B: 2 or 4
   int mc = 1;
-  if (!no_mc) {
+  if (!no_mc && (force_mc == 2 || force_mc == 4) && tiles % force_mc == 0) {
+    mc = force_mc;
+  } else if (!no_mc) {
     int64_t best = -1;
     for (int m : {4, 2}) {
       if (tiles % m != 0) continue;
